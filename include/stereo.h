@@ -1,0 +1,196 @@
+/* include/stereo.h — C ABI of the B200-native stereo hot path.
+ *
+ * Implements the data-parallel pipeline of Chang & Maruyama, "Real-Time
+ * High-Quality Stereo Matching System on a GPU" (arXiv 2212.00488), §III and
+ * §IV Steps 1-8, as hand-written CUDA kernels for sm_100a:
+ *
+ *   SD (Eq. 2)  -> mini-census + cross arms
+ *   -> cost + x aggregation, both bases (Eqs. 3-7; Step3 P:418-457)
+ *   -> y aggregation + WTA, both bases (Eqs. 8-9; Step5 P:474-502)
+ *   -> cross-check (Eq. 10) + 3x3 median (Step7)
+ *   -> bilateral fill of non-GCPs (§III.E; Step7 P:516-525)
+ *   -> bilateral/linear scale-up (Step8)
+ *
+ * Plain C linkage: no C++ types, no torch types, no exceptions cross this
+ * boundary.  Pointers are either DEVICE pointers (cudaMalloc'd or torch CUDA
+ * tensor storage on the handle's device) or HOST pointers, as stated per call.
+ * Streams are passed as `void*` holding a cudaStream_t (NULL = legacy default
+ * stream).
+ *
+ * Numerics (DESIGN.md §2 reading R12c): every cost term is quantised once to
+ * fixed point, Q = floor(c * 2^f + 0.5), f = largest value <= 25 with
+ * (2 w_x + 1) 2^(f+1) < 2^32; all aggregation is then exact integer arithmetic
+ * (u32 modular prefix sums along x, u64 along y), so the result is bit-exact
+ * with the CPU oracle's fixed mode and within 0.5*2^-f/c_AD(1) <= 1.2e-6
+ * relative of the IEEE-double definition on every aggregated cost.
+ *
+ * Errors: every function returns STEREO_OK (0) or a negative STEREO_E* code and
+ * never aborts; stereo_last_error() returns a thread-local message naming the
+ * first violated invariant or the failing CUDA call.  Asynchronous kernel
+ * faults surface at the caller's next synchronisation of the stream.
+ */
+#ifndef STEREO_B200_H
+#define STEREO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STEREO_ABI_VERSION 1u
+
+enum {
+  STEREO_OK = 0,
+  STEREO_EINVAL = -1,       /* invalid argument / parameter invariant violated */
+  STEREO_ENOMEM = -2,       /* device or host allocation failed */
+  STEREO_ECUDA = -3,        /* a CUDA runtime call or launch failed */
+  STEREO_EUNSUPPORTED = -4  /* valid per the paper, outside this build's limits */
+};
+
+/* Method parameters.  Defaults (stereo_default_params) are the paper's values
+ * where it gives them: lambda_AD = 0.3, lambda_MC = 2.3, T = 3,
+ * W_x = 21, W_y = 31, K = 2, 3x3 mean pool;
+ * delta = 20 (the paper never states it, reading R13);
+ * census pattern (0,-2)(-1,-1)(+1,-1)(-1,+1)(+1,+1)(0,+2) (Fig. 3 is missing;
+ * SPEC S:92, reading R8). */
+typedef struct {
+  uint32_t abi_version;  /* must equal STEREO_ABI_VERSION */
+  double lambda_ad;      /* Eq. 4 scale; AD uses |dI|/255 (reading R12), > 0 */
+  double lambda_mc;      /* Eq. 5 scale on the raw Hamming distance, > 0 */
+  int32_t t_fill;        /* T: continuity threshold of §III.E; SU uses K*T; >= 0 */
+  int32_t w_x, w_y;      /* per-side arm caps W_x, W_y; 0..254 */
+  int32_t delta;         /* arm similarity |dI| < delta (strict); > 0 */
+  int32_t k_scale;       /* K: 2 (scale down/up) or 1 (no scaling path) */
+  int32_t m_pool;        /* mean-pool radius m of Eq. 2; 0..3 */
+  int8_t census_dx[6];   /* the six mini-census offsets, |dx|,|dy| <= 2, */
+  int8_t census_dy[6];   /* distinct and non-zero; bit i <-> offset i */
+} stereo_params;
+
+/* Derived sizes and resources of a handle (filled by stereo_get_info). */
+typedef struct {
+  int32_t W, H, D;        /* original width, height, maximum disparity */
+  int32_t Ws, Hs, Ds;     /* scaled: W/K, H/K (floor), ceil(D/K) */
+  int32_t frac_bits;      /* f of the fixed-point cost */
+  int32_t device;         /* CUDA device ordinal the handle is bound to */
+  uint64_t device_bytes;  /* total device scratch owned by the handle */
+  uint64_t cax_bytes;     /* bytes of ONE CA_x volume (u32 [Ds][Hs][cax_pitch]) */
+  int32_t launches_per_frame; /* kernels enqueued by one stereo_compute */
+  int32_t ypass_block_rows;   /* output rows per y-aggregation tile */
+  int32_t cax_pitch;          /* row pitch (elements) of the CA_x volumes */
+} stereo_info;
+
+typedef struct stereo_s stereo_t; /* opaque; owns ALL device scratch */
+
+/* Fill *p with the defaults above.  p must be non-NULL. */
+void stereo_default_params(stereo_params* p);
+
+/* Create a handle for W x H u8 gray inputs and maximum disparity D (candidates
+ * d = 0..D-1) at ORIGINAL resolution, on the current CUDA device.
+ * Validates, in order: lambda_ad > 0, lambda_mc > 0, delta > 0,
+ * t_fill >= 0, w_x >= 0, w_y >= 0, k_scale >= 1, D >= 1, W >= 1, H >= 1,
+ * W/K >= 1, H/K >= 1, six distinct non-zero census offsets -> STEREO_EINVAL.
+ * STEREO_EUNSUPPORTED for K not in {1,2}, ceil(D/K) > 255 (u8 maps use 255 as
+ * INVALID), w_x or w_y > 254 (u8 arms), census offsets beyond +-2, m_pool > 3.
+ * Allocates every device buffer (dominant: two u32 CA_x volumes of
+ * Ds*Hs*Ws*4 bytes each), builds the fixed-point cost tables on the host in
+ * double precision and uploads them.  No kernel runs.  On success *out owns
+ * the handle (release with stereo_destroy). */
+int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out);
+
+/* Enqueue one frame on `stream` and return without synchronising.
+ * L, R: DEVICE u8 [H][W], row pitch W (rectified left/right gray images).
+ * disp_out: DEVICE f32 [H][W], receives D^{fL_org}, the left-based
+ * disparity in original-resolution pixels, range [0, K*(Ds-1)]; every pixel is
+ * written, INVALID is never emitted.  L, R and disp_out stay owned by the
+ * caller and must remain valid until the stream work completes.  A handle is
+ * not re-entrant: use one handle per concurrently running stream. */
+int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
+                   void* stream);
+
+/* `nframes` frames back to back; L, R: DEVICE u8 [nframes][H][W]; disp_out:
+ * DEVICE f32 [nframes][H][W].  Same contract as stereo_compute. */
+int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
+                         float* disp_out, void* stream);
+
+/* End-to-end variant with HOST buffers: copies L and R (HOST u8 [H][W]) into
+ * handle-owned device staging, computes, copies the result into disp_out
+ * (HOST f32 [H][W]), all enqueued on `stream`; returns without synchronising.
+ * Host buffers should be page-locked (cudaHostAlloc / torch pin_memory) for
+ * the copies to be asynchronous; the caller must synchronise the stream
+ * before reading disp_out or reusing L/R. */
+int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
+                        void* stream);
+
+/* Synchronise the device, then free every buffer and the handle.  NULL is a
+ * no-op. */
+void stereo_destroy(stereo_t* h);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* stereo_last_error(void);
+
+int stereo_get_info(const stereo_t* h, stereo_info* info);
+
+/* Copy the handle's fixed-point tables to HOST arrays: qad[256] (indexed by
+ * |dI|), qmc[7] (indexed by Hamming distance); *border = 2^(f+1). */
+int stereo_get_tables(const stereo_t* h, uint32_t* qad, uint32_t* qmc, uint32_t* border);
+
+/* ---- stage-level access (parity tests, profiling) ------------------------
+ * Buffer ids and their layouts (all row-major, scaled resolution unless noted):
+ *   STEREO_BUF_PIX_L/R : u16 [Hs][Ws]  = I | census << 8  (scaled image + code)
+ *   STEREO_BUF_ARM_L/R : u32 [Hs][Ws]  = m | n << 8 | M << 16 | N << 24
+ *                        (m, n: -x/+x arms; M, N: -y/+y arms)
+ *   STEREO_BUF_CAX_L/R : u32 [Ds][Hs][Wp]  Eq. 7 (fixed point); Wp = cax_pitch
+ *                        = Ws rounded up to 32 (columns >= Ws are undefined)
+ *   STEREO_BUF_CA_L/R  : u64 [Ds][Hs][Ws]  Eq. 8, only after
+ *                        stereo_set_debug(h, STEREO_DEBUG_CA, 1)
+ *   STEREO_BUF_DL/DR   : u8  [Hs][Ws]  Eq. 9 WTA maps
+ *   STEREO_BUF_MASKED  : u8  [Hs][Ws]  D^L with non-GCPs = 255 (Eq. 10)
+ *   STEREO_BUF_MEDIAN  : u8  [Hs][Ws]  after the 3x3 median
+ *   STEREO_BUF_FILL    : f32 [Hs][Ws]  D^{+L}
+ * stereo_debug_download synchronises the device; `bytes` must equal the
+ * buffer size exactly (STEREO_EINVAL otherwise). */
+enum {
+  STEREO_BUF_PIX_L = 0, STEREO_BUF_PIX_R, STEREO_BUF_ARM_L, STEREO_BUF_ARM_R,
+  STEREO_BUF_CAX_L, STEREO_BUF_CAX_R, STEREO_BUF_CA_L, STEREO_BUF_CA_R,
+  STEREO_BUF_DL, STEREO_BUF_DR, STEREO_BUF_MASKED, STEREO_BUF_MEDIAN,
+  STEREO_BUF_FILL, STEREO_BUF_COUNT
+};
+int stereo_debug_download(stereo_t* h, int buf_id, void* host_dst, size_t bytes);
+int stereo_debug_upload(stereo_t* h, int buf_id, const void* host_src, size_t bytes);
+
+/* Debug switches: STEREO_DEBUG_CA (allocate + store the CA volumes). */
+enum { STEREO_DEBUG_CA = 1 };
+int stereo_set_debug(stereo_t* h, int what, int enable);
+
+/* Run ONE stage on the handle's buffers (after stereo_debug_upload of its
+ * inputs).  L, R: DEVICE u8 [H][W] originals (used by SD and, for K = 1, by
+ * PREP); disp_out: DEVICE f32 [H][W] (written by SU; by FILL when K = 1).
+ * Stage ids follow the paper's Table II taxonomy. */
+enum {
+  STEREO_STAGE_SD = 0,     /* Eq. 2 (K = 2 only; no-op for K = 1) */
+  STEREO_STAGE_PREP,       /* census + x/y arms: Table II W^{LR}_+-, W^{*LR}_+- */
+  STEREO_STAGE_XPASS,      /* C + CA_x */
+  STEREO_STAGE_YPASS,      /* CA + WTA */
+  STEREO_STAGE_CCMED,      /* CC + median */
+  STEREO_STAGE_FILL,       /* bilateral fill (Post) */
+  STEREO_STAGE_SU,         /* scale-up (K = 2 only) */
+  STEREO_STAGE_COUNT
+};
+int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,
+                     float* disp_out, void* stream);
+
+/* Per-stage device timing with CUDA events recorded on the compute stream.
+ * stereo_set_timing(h, 1) resets the accumulators and starts recording around
+ * every stage of every subsequent stereo_compute*; stereo_stage_times_ms
+ * synchronises on the recorded events and returns, per stage id, the summed
+ * milliseconds over *nframes frames recorded since the reset. */
+int stereo_set_timing(stereo_t* h, int enable);
+int stereo_stage_times_ms(stereo_t* h, double* ms_per_stage /* [STEREO_STAGE_COUNT] */,
+                          int* nframes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STEREO_B200_H */

@@ -1,0 +1,260 @@
+"""Thin ctypes binding of include/stereo.h (argument marshalling only).
+
+Every function here forwards to the same-named C entry point of
+``paper_2212_00488_b200/lib/libstereo_b200.so``; all computation happens in
+that library's sm_100a kernels.  There is no CPU fallback: if the library is
+missing or cannot be loaded, :func:`lib` raises ``StereoLibraryError``.
+
+Device buffers are passed as raw pointers; :class:`Stereo` accepts torch CUDA
+tensors (PyTorch supplies device memory and streams only) and numpy arrays
+for the host (end-to-end) path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("STEREO_B200_LIB", os.path.join(_HERE, "lib", "libstereo_b200.so"))
+
+STEREO_ABI_VERSION = 1
+STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, -1, -2, -3, -4
+
+(BUF_PIX_L, BUF_PIX_R, BUF_ARM_L, BUF_ARM_R, BUF_CAX_L, BUF_CAX_R, BUF_CA_L, BUF_CA_R,
+ BUF_DL, BUF_DR, BUF_MASKED, BUF_MEDIAN, BUF_FILL) = range(13)
+(STAGE_SD, STAGE_PREP, STAGE_XPASS, STAGE_YPASS, STAGE_CCMED, STAGE_FILL, STAGE_SU) = range(7)
+STAGE_NAMES = ("SD", "PREP", "XPASS", "YPASS", "CCMED", "FILL", "SU")
+STAGE_COUNT = 7
+DEBUG_CA = 1
+
+# every symbol include/stereo.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "stereo_default_params", "stereo_create", "stereo_compute", "stereo_compute_batch",
+    "stereo_compute_host", "stereo_destroy", "stereo_last_error", "stereo_get_info",
+    "stereo_get_tables", "stereo_debug_download", "stereo_debug_upload", "stereo_set_debug",
+    "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms",
+)
+
+
+class StereoLibraryError(RuntimeError):
+    pass
+
+
+class StereoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"stereo error {code}: {msg}")
+        self.code = code
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_uint32), ("lambda_ad", C.c_double), ("lambda_mc", C.c_double),
+        ("t_fill", C.c_int32), ("w_x", C.c_int32), ("w_y", C.c_int32), ("delta", C.c_int32),
+        ("k_scale", C.c_int32), ("m_pool", C.c_int32),
+        ("census_dx", C.c_int8 * 6), ("census_dy", C.c_int8 * 6),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("W", C.c_int32), ("H", C.c_int32), ("D", C.c_int32),
+        ("Ws", C.c_int32), ("Hs", C.c_int32), ("Ds", C.c_int32),
+        ("frac_bits", C.c_int32), ("device", C.c_int32),
+        ("device_bytes", C.c_uint64), ("cax_bytes", C.c_uint64),
+        ("launches_per_frame", C.c_int32), ("ypass_block_rows", C.c_int32),
+        ("cax_pitch", C.c_int32),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libstereo_b200.so (raises StereoLibraryError if absent: no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise StereoLibraryError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (or tools/build_lib.sh); there is no CPU fallback")
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as e:
+            raise StereoLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+        vp, i32 = C.c_void_p, C.c_int
+        sig = {
+            "stereo_default_params": (None, [C.POINTER(Params)]),
+            "stereo_create": (i32, [i32, i32, i32, C.POINTER(Params), C.POINTER(vp)]),
+            "stereo_compute": (i32, [vp, vp, vp, vp, vp]),
+            "stereo_compute_batch": (i32, [vp, vp, vp, i32, vp, vp]),
+            "stereo_compute_host": (i32, [vp, vp, vp, vp, vp]),
+            "stereo_destroy": (None, [vp]),
+            "stereo_last_error": (C.c_char_p, []),
+            "stereo_get_info": (i32, [vp, C.POINTER(Info)]),
+            "stereo_get_tables": (i32, [vp, vp, vp, vp]),
+            "stereo_debug_download": (i32, [vp, i32, vp, C.c_size_t]),
+            "stereo_debug_upload": (i32, [vp, i32, vp, C.c_size_t]),
+            "stereo_set_debug": (i32, [vp, i32, i32]),
+            "stereo_run_stage": (i32, [vp, i32, vp, vp, vp, vp]),
+            "stereo_set_timing": (i32, [vp, i32]),
+            "stereo_stage_times_ms": (i32, [vp, vp, C.POINTER(C.c_int)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+        return L
+
+
+def _check(rc):
+    if rc != STEREO_OK:
+        raise StereoError(rc, lib().stereo_last_error().decode(errors="replace"))
+
+
+def default_params(**overrides) -> Params:
+    p = Params()
+    lib().stereo_default_params(C.byref(p))
+    census = overrides.pop("census", None)
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    if census is not None:
+        for i, (dx, dy) in enumerate(census):
+            p.census_dx[i], p.census_dy[i] = dx, dy
+    return p
+
+
+def _ptr(t):
+    """Raw pointer of a torch tensor / numpy array / int."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensors must be contiguous"
+    return t.data_ptr()
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Stereo:
+    """Owns one stereo_t handle (device-bound; not re-entrant across streams)."""
+
+    def __init__(self, W: int, H: int, D: int, params: Params | None = None, **overrides):
+        self.params = params if params is not None else default_params(**overrides)
+        h = C.c_void_p()
+        _check(lib().stereo_create(W, H, D, C.byref(self.params), C.byref(h)))
+        self._h = h
+        self.info = Info()
+        _check(lib().stereo_get_info(self._h, C.byref(self.info)))
+        self.W, self.H, self.D = W, H, D
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().stereo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------ compute
+    def compute(self, L, R, out, stream=None):
+        """L, R: CUDA u8 [H][W]; out: CUDA f32 [H][W]. Enqueued, not synchronised."""
+        _check(lib().stereo_compute(self._h, _ptr(L), _ptr(R), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def compute_batch(self, L, R, out, nframes, stream=None):
+        _check(lib().stereo_compute_batch(self._h, _ptr(L), _ptr(R), nframes, _ptr(out),
+                                          _stream_ptr(stream)))
+        return out
+
+    def compute_host(self, L, R, out, stream=None):
+        """HOST buffers (pinned for async copies); caller synchronises the stream."""
+        _check(lib().stereo_compute_host(self._h, _ptr(L), _ptr(R), _ptr(out),
+                                         _stream_ptr(stream)))
+        return out
+
+    # ------------------------------------------------------------ debug / stages
+    def tables(self):
+        qad = np.zeros(256, np.uint32)
+        qmc = np.zeros(7, np.uint32)
+        border = C.c_uint32()
+        _check(lib().stereo_get_tables(self._h, qad.ctypes.data, qmc.ctypes.data, C.byref(border)))
+        return qad, qmc, border.value
+
+    def _shape(self, buf):
+        i = self.info
+        n2 = (i.Hs, i.Ws)
+        return {
+            BUF_PIX_L: (n2, np.uint16), BUF_PIX_R: (n2, np.uint16),
+            BUF_ARM_L: (n2, np.uint32), BUF_ARM_R: (n2, np.uint32),
+            BUF_CAX_L: ((i.Ds, i.Hs, i.cax_pitch), np.uint32),
+            BUF_CAX_R: ((i.Ds, i.Hs, i.cax_pitch), np.uint32),
+            BUF_CA_L: ((i.Ds, i.Hs, i.Ws), np.uint64), BUF_CA_R: ((i.Ds, i.Hs, i.Ws), np.uint64),
+            BUF_DL: (n2, np.uint8), BUF_DR: (n2, np.uint8), BUF_MASKED: (n2, np.uint8),
+            BUF_MEDIAN: (n2, np.uint8), BUF_FILL: (n2, np.float32),
+        }[buf]
+
+    def download(self, buf):
+        shp, dt = self._shape(buf)
+        a = np.zeros(shp, dt)
+        _check(lib().stereo_debug_download(self._h, buf, a.ctypes.data, a.nbytes))
+        return a
+
+    def upload(self, buf, arr):
+        shp, dt = self._shape(buf)
+        a = np.ascontiguousarray(arr, dtype=dt).reshape(shp)
+        _check(lib().stereo_debug_upload(self._h, buf, a.ctypes.data, a.nbytes))
+
+    def set_debug(self, what, enable=True):
+        _check(lib().stereo_set_debug(self._h, what, int(enable)))
+
+    def run_stage(self, stage, L=None, R=None, out=None, stream=None):
+        _check(lib().stereo_run_stage(self._h, stage, _ptr(L), _ptr(R), _ptr(out),
+                                      _stream_ptr(stream)))
+
+    def set_timing(self, enable=True):
+        _check(lib().stereo_set_timing(self._h, int(enable)))
+
+    def stage_times_ms(self):
+        ms = np.zeros(STAGE_COUNT, np.float64)
+        n = C.c_int()
+        _check(lib().stereo_stage_times_ms(self._h, ms.ctypes.data, C.byref(n)))
+        return dict(zip(STAGE_NAMES, ms.tolist())), n.value
+
+
+def unpack_pix(pix):
+    """u16 I | census << 8 -> (image u8, census u8)."""
+    return (pix & 255).astype(np.uint8), (pix >> 8).astype(np.uint8)
+
+
+def unpack_arms(arm):
+    """u32 m | n<<8 | M<<16 | N<<24 -> u8 [4][H][W] (m, n, M, N)."""
+    return np.stack([(arm >> s) & 255 for s in (0, 8, 16, 24)]).astype(np.uint8)

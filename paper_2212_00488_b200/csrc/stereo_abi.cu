@@ -1,0 +1,491 @@
+// stereo_abi.cu — host side of the C ABI declared in include/stereo.h.
+//
+// Owns validation (SPEC S:59-61 order), the fixed-point table builder, the
+// buffer planner, the per-frame launch sequence (Step1..Step8 order)
+// and the CUDA-event stage timers.  No kernel runs at create time.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stereo.h"
+#include "stereo_internal.cuh"
+
+using namespace stereo;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                 \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(e_ == cudaErrorMemoryAllocation ? STEREO_ENOMEM : STEREO_ECUDA, \
+                  "%s: %s", #call, cudaGetErrorString(e_));                      \
+  } while (0)
+
+struct TimedFrame {
+  cudaEvent_t ev[STEREO_STAGE_COUNT + 1];
+  int stage[STEREO_STAGE_COUNT];
+  int n;
+};
+}  // namespace
+
+struct stereo_s {
+  Geom g{};
+  Plan plan{};
+  Buffers b{};
+  stereo_params params{};
+  int device = 0;
+  bool debug_ca = false;
+  uint32_t qad_h[256];
+  uint32_t qmc_h[7];
+  std::vector<void*> allocs;
+  // timing
+  bool timing = false;
+  std::vector<TimedFrame> pending;
+  std::vector<cudaEvent_t> pool;
+  double acc_ms[STEREO_STAGE_COUNT] = {0};
+  int acc_frames = 0;
+};
+
+namespace {
+
+int alloc(stereo_t* h, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    return fail(STEREO_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+  h->allocs.push_back(*p);
+  return STEREO_OK;
+}
+
+// Eq. 4 / Eq. 5 evaluated in IEEE double, then quantised once:
+// Q = floor(c * 2^f + 0.5)  (reading R12c).
+void build_tables(const stereo_params& p, int f, uint32_t qad[256], uint32_t qmc[7]) {
+  const double scale = std::ldexp(1.0, f);
+  for (int a = 0; a < 256; ++a) {
+    const double c = 1.0 - std::exp(-((static_cast<double>(a) / 255.0) / p.lambda_ad));
+    qad[a] = static_cast<uint32_t>(std::floor(c * scale + 0.5));
+  }
+  for (int k = 0; k < 7; ++k) {
+    const double c = 1.0 - std::exp(-(static_cast<double>(k) / p.lambda_mc));
+    qmc[k] = static_cast<uint32_t>(std::floor(c * scale + 0.5));
+  }
+}
+
+int frac_bits(int w_x) {
+  for (int f = 25; f >= 0; --f)
+    if ((static_cast<uint64_t>(2 * w_x + 1) << (f + 1)) < (1ull << 32)) return f;
+  return -1;
+}
+
+int validate(int W, int H, int D, const stereo_params* p) {
+  if (!p) return fail(STEREO_EINVAL, "params must not be NULL");
+  if (p->abi_version != STEREO_ABI_VERSION)
+    return fail(STEREO_EINVAL, "abi_version %u != %u", p->abi_version, STEREO_ABI_VERSION);
+  if (!(p->lambda_ad > 0)) return fail(STEREO_EINVAL, "lambda_ad must be > 0");
+  if (!(p->lambda_mc > 0)) return fail(STEREO_EINVAL, "lambda_mc must be > 0");
+  if (p->delta <= 0) return fail(STEREO_EINVAL, "delta must be > 0");
+  if (p->t_fill < 0) return fail(STEREO_EINVAL, "t_fill must be >= 0");
+  if (p->w_x < 0) return fail(STEREO_EINVAL, "w_x must be >= 0");
+  if (p->w_y < 0) return fail(STEREO_EINVAL, "w_y must be >= 0");
+  if (p->k_scale < 1) return fail(STEREO_EINVAL, "k_scale must be >= 1");
+  if (D < 1) return fail(STEREO_EINVAL, "D (d_max_org) must be >= 1");
+  if (W < 1 || H < 1) return fail(STEREO_EINVAL, "W and H must be >= 1");
+  if (p->m_pool < 0) return fail(STEREO_EINVAL, "m_pool must be >= 0");
+  for (int i = 0; i < 6; ++i) {
+    if (p->census_dx[i] == 0 && p->census_dy[i] == 0)
+      return fail(STEREO_EINVAL, "census offset %d is zero", i);
+    for (int j = 0; j < i; ++j)
+      if (p->census_dx[i] == p->census_dx[j] && p->census_dy[i] == p->census_dy[j])
+        return fail(STEREO_EINVAL, "census offsets %d and %d are not distinct", j, i);
+  }
+  if (p->k_scale > 2) return fail(STEREO_EUNSUPPORTED, "k_scale must be 1 or 2");
+  if (W / p->k_scale < 1 || H / p->k_scale < 1)
+    return fail(STEREO_EINVAL, "scaled image is empty (W/K or H/K < 1)");
+  if ((D + p->k_scale - 1) / p->k_scale > 255)
+    return fail(STEREO_EUNSUPPORTED, "ceil(D/K) must be <= 255 (u8 disparity maps)");
+  if (p->w_x > 254 || p->w_y > 254) return fail(STEREO_EUNSUPPORTED, "w_x, w_y must be <= 254");
+  if (p->m_pool > 3) return fail(STEREO_EUNSUPPORTED, "m_pool must be <= 3");
+  for (int i = 0; i < 6; ++i)
+    if (p->census_dx[i] < -2 || p->census_dx[i] > 2 || p->census_dy[i] < -2 || p->census_dy[i] > 2)
+      return fail(STEREO_EUNSUPPORTED, "census offsets must lie within +-2");
+  return STEREO_OK;
+}
+
+cudaEvent_t get_event(stereo_t* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+int drain_one(stereo_t* h, size_t idx) {
+  TimedFrame& f = h->pending[idx];
+  CU(cudaEventSynchronize(f.ev[f.n]));
+  for (int i = 0; i < f.n; ++i) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, f.ev[i], f.ev[i + 1]));
+    h->acc_ms[f.stage[i]] += ms;
+  }
+  for (int i = 0; i <= f.n; ++i) h->pool.push_back(f.ev[i]);
+  h->acc_frames += 1;
+  return STEREO_OK;
+}
+
+// One frame: the Step1..Step8 launch sequence.
+int enqueue_frame(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, cudaStream_t s) {
+  const Geom& g = h->g;
+  Buffers& b = h->b;
+  TimedFrame tf{};
+  if (h->timing) {
+    tf.ev[0] = get_event(h);
+    cudaEventRecord(tf.ev[0], s);
+  }
+  auto mark = [&](int stage) {
+    if (!h->timing) return;
+    tf.stage[tf.n] = stage;
+    tf.ev[tf.n + 1] = get_event(h);
+    cudaEventRecord(tf.ev[tf.n + 1], s);
+    tf.n += 1;
+  };
+  const uint8_t* Ls = L;
+  const uint8_t* Rs = R;
+  if (g.K == 2) {
+    CU(launch_sd(g, L, R, b.Ls, b.Rs, s));
+    mark(STEREO_STAGE_SD);
+    Ls = b.Ls;
+    Rs = b.Rs;
+  }
+  CU(launch_prep(g, Ls, Rs, b, s));
+  mark(STEREO_STAGE_PREP);
+  CU(launch_xpass(g, h->plan, b, s));
+  mark(STEREO_STAGE_XPASS);
+  CU(launch_ypass(g, h->plan, b, h->debug_ca, s));
+  mark(STEREO_STAGE_YPASS);
+  CU(launch_ccmed(g, b, s));
+  mark(STEREO_STAGE_CCMED);
+  CU(launch_fill(g, b, g.K == 2 ? b.fill : out, s));
+  mark(STEREO_STAGE_FILL);
+  if (g.K == 2) {
+    CU(launch_su(g, b.fill, L, out, s));
+    mark(STEREO_STAGE_SU);
+  }
+  if (h->timing) {
+    h->pending.push_back(tf);
+    if (h->pending.size() > 4096) {  // bound the event pool; the GPU is far behind anyway
+      int rc = drain_one(h, 0);
+      h->pending.erase(h->pending.begin());
+      if (rc) return rc;
+    }
+  }
+  return STEREO_OK;
+}
+
+struct BufView {
+  void* p;
+  size_t bytes;
+};
+
+BufView buf_view(stereo_t* h, int id) {
+  const Geom& g = h->g;
+  const size_t n = (size_t)g.Ws * g.Hs;
+  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  switch (id) {
+    case STEREO_BUF_PIX_L: return {h->b.pixL, n * 2};
+    case STEREO_BUF_PIX_R: return {h->b.pixR, n * 2};
+    case STEREO_BUF_ARM_L: return {h->b.armL, n * 4};
+    case STEREO_BUF_ARM_R: return {h->b.armR, n * 4};
+    case STEREO_BUF_CAX_L: return {h->b.caxL, vol * 4};
+    case STEREO_BUF_CAX_R: return {h->b.caxR, vol * 4};
+    case STEREO_BUF_CA_L: return {h->b.caL, h->b.caL ? n * g.Ds * 8 : 0};
+    case STEREO_BUF_CA_R: return {h->b.caR, h->b.caR ? n * g.Ds * 8 : 0};
+    case STEREO_BUF_DL: return {h->b.DL, n};
+    case STEREO_BUF_DR: return {h->b.DR, n};
+    case STEREO_BUF_MASKED: return {h->b.masked, n};
+    case STEREO_BUF_MEDIAN: return {h->b.median, n};
+    case STEREO_BUF_FILL: return {h->b.fill, n * 4};
+    default: return {nullptr, 0};
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void stereo_default_params(stereo_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof *p);
+  p->abi_version = STEREO_ABI_VERSION;
+  p->lambda_ad = 0.3;
+  p->lambda_mc = 2.3;
+  p->t_fill = 3;
+  p->w_x = 21;
+  p->w_y = 31;
+  p->delta = 20;
+  p->k_scale = 2;
+  p->m_pool = 1;
+  const int8_t dx[6] = {0, -1, 1, -1, 1, 0}, dy[6] = {-2, -1, -1, 1, 1, 2};
+  for (int i = 0; i < 6; ++i) {
+    p->census_dx[i] = dx[i];
+    p->census_dy[i] = dy[i];
+  }
+}
+
+const char* stereo_last_error(void) { return g_err.c_str(); }
+
+int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
+  g_err.clear();
+  if (!out) return fail(STEREO_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  int rc = validate(W, H, D, p);
+  if (rc) return rc;
+  stereo_t* h = new (std::nothrow) stereo_t();
+  if (!h) return fail(STEREO_ENOMEM, "host allocation failed");
+  h->params = *p;
+  Geom& g = h->g;
+  g.W = W; g.H = H; g.D = D; g.K = p->k_scale; g.m_pool = p->m_pool;
+  g.Ws = W / g.K; g.Hs = H / g.K; g.Ds = (D + g.K - 1) / g.K;
+  g.Wp = (g.Ws + 31) / 32 * 32;
+  g.w_x = p->w_x; g.w_y = p->w_y; g.delta = p->delta; g.t_fill = p->t_fill;
+  g.f = frac_bits(p->w_x);
+  g.border = 1u << (g.f + 1);
+  for (int i = 0; i < 6; ++i) { g.cdx[i] = p->census_dx[i]; g.cdy[i] = p->census_dy[i]; }
+  if (!xpass_chunk_for(g.Ws)) {
+    delete h;
+    return fail(STEREO_EUNSUPPORTED, "scaled width %d exceeds 2016", g.Ws);
+  }
+  if (g.w_y > 124) {
+    delete h;
+    return fail(STEREO_EUNSUPPORTED, "w_y > 124 not supported by the y-aggregation tile");
+  }
+  cudaError_t e = cudaGetDevice(&h->device);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(STEREO_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  }
+  build_tables(*p, g.f, h->qad_h, h->qmc_h);
+  const size_t n = (size_t)g.Ws * g.Hs;
+  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  Buffers& b = h->b;
+  struct A { void** p; size_t bytes; } as[] = {
+      {(void**)&b.pixL, n * 2}, {(void**)&b.pixR, n * 2}, {(void**)&b.armL, n * 4},
+      {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
+      {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
+      {(void**)&b.rowFirst, (size_t)g.Hs * 4}, {(void**)&b.rowLast, (size_t)g.Hs * 4},
+      {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
+  };
+  for (auto& a : as) {
+    if ((rc = alloc(h, a.p, a.bytes))) { stereo_destroy(h); return rc; }
+  }
+  if (g.K == 2) {
+    if ((rc = alloc(h, (void**)&b.Ls, n)) || (rc = alloc(h, (void**)&b.Rs, n))) {
+      stereo_destroy(h);
+      return rc;
+    }
+  }
+  e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(b.qmc, h->qmc_h, sizeof h->qmc_h, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = plan_kernels(g, h->plan, h->device);
+  if (e != cudaSuccess) {
+    stereo_destroy(h);
+    return fail(STEREO_ECUDA, "setup: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return STEREO_OK;
+}
+
+void stereo_destroy(stereo_t* h) {
+  if (!h) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (auto& f : h->pending)
+    for (int i = 0; i <= f.n; ++i) cudaEventDestroy(f.ev[i]);
+  for (auto e : h->pool) cudaEventDestroy(e);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->b.caL) cudaFree(h->b.caL);
+  if (h->b.caR) cudaFree(h->b.caR);
+  cudaSetDevice(cur);
+  delete h;
+}
+
+int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
+                   void* stream) {
+  if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  return enqueue_frame(h, L, R, disp_out, (cudaStream_t)stream);
+}
+
+int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
+                         float* disp_out, void* stream) {
+  if (!h || !L || !R || !disp_out || nframes < 0)
+    return fail(STEREO_EINVAL, "NULL handle/buffer or negative nframes");
+  const size_t in = (size_t)h->g.W * h->g.H;
+  for (int i = 0; i < nframes; ++i) {
+    int rc = enqueue_frame(h, L + i * in, R + i * in, disp_out + i * in, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return STEREO_OK;
+}
+
+int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
+                        void* stream) {
+  if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  const size_t in = (size_t)h->g.W * h->g.H;
+  int rc;
+  if (!h->b.inL) {
+    if ((rc = alloc(h, (void**)&h->b.inL, in)) || (rc = alloc(h, (void**)&h->b.inR, in)) ||
+        (rc = alloc(h, (void**)&h->b.outF, in * 4)))
+      return rc;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(h->b.inL, L, in, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h->b.inR, R, in, cudaMemcpyHostToDevice, s));
+  if ((rc = enqueue_frame(h, h->b.inL, h->b.inR, h->b.outF, s))) return rc;
+  CU(cudaMemcpyAsync(disp_out, h->b.outF, in * 4, cudaMemcpyDeviceToHost, s));
+  return STEREO_OK;
+}
+
+int stereo_get_info(const stereo_t* h, stereo_info* info) {
+  if (!h || !info) return fail(STEREO_EINVAL, "NULL handle or info");
+  const Geom& g = h->g;
+  info->W = g.W; info->H = g.H; info->D = g.D;
+  info->Ws = g.Ws; info->Hs = g.Hs; info->Ds = g.Ds;
+  info->frac_bits = g.f;
+  info->device = h->device;
+  uint64_t tot = 0;
+  const size_t n = (size_t)g.Ws * g.Hs;
+  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  tot += n * (2 + 2 + 4 + 4 + 1 + 1 + 1 + 1 + 4) + vol * 8 + (size_t)g.Hs * 8 + 263 * 4;
+  if (g.K == 2) tot += 2 * n;
+  info->device_bytes = tot;
+  info->cax_bytes = vol * 4;
+  info->launches_per_frame = g.K == 2 ? 7 : 5;
+  info->ypass_block_rows = h->plan.ypass_B;
+  info->cax_pitch = g.Wp;
+  return STEREO_OK;
+}
+
+int stereo_get_tables(const stereo_t* h, uint32_t* qad, uint32_t* qmc, uint32_t* border) {
+  if (!h || !qad || !qmc || !border) return fail(STEREO_EINVAL, "NULL argument");
+  std::memcpy(qad, h->qad_h, sizeof h->qad_h);
+  std::memcpy(qmc, h->qmc_h, sizeof h->qmc_h);
+  *border = h->g.border;
+  return STEREO_OK;
+}
+
+int stereo_debug_download(stereo_t* h, int buf_id, void* host_dst, size_t bytes) {
+  if (!h || !host_dst) return fail(STEREO_EINVAL, "NULL argument");
+  BufView v = buf_view(h, buf_id);
+  if (!v.p) return fail(STEREO_EINVAL, "buffer %d not available", buf_id);
+  if (bytes != v.bytes) return fail(STEREO_EINVAL, "buffer %d has %zu bytes, not %zu", buf_id, v.bytes, bytes);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(host_dst, v.p, bytes, cudaMemcpyDeviceToHost));
+  return STEREO_OK;
+}
+
+int stereo_debug_upload(stereo_t* h, int buf_id, const void* host_src, size_t bytes) {
+  if (!h || !host_src) return fail(STEREO_EINVAL, "NULL argument");
+  BufView v = buf_view(h, buf_id);
+  if (!v.p) return fail(STEREO_EINVAL, "buffer %d not available", buf_id);
+  if (bytes != v.bytes) return fail(STEREO_EINVAL, "buffer %d has %zu bytes, not %zu", buf_id, v.bytes, bytes);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(v.p, host_src, bytes, cudaMemcpyHostToDevice));
+  return STEREO_OK;
+}
+
+int stereo_set_debug(stereo_t* h, int what, int enable) {
+  if (!h) return fail(STEREO_EINVAL, "NULL handle");
+  if (what != STEREO_DEBUG_CA) return fail(STEREO_EINVAL, "unknown debug switch %d", what);
+  if (enable && !h->b.caL) {
+    const size_t bytes = (size_t)h->g.Ds * h->g.Hs * h->g.Ws * 8;
+    CU(cudaMalloc(&h->b.caL, bytes));
+    CU(cudaMalloc(&h->b.caR, bytes));
+  }
+  h->debug_ca = enable != 0;
+  return STEREO_OK;
+}
+
+int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,
+                     float* disp_out, void* stream) {
+  if (!h) return fail(STEREO_EINVAL, "NULL handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Geom& g = h->g;
+  Buffers& b = h->b;
+  switch (stage_id) {
+    case STEREO_STAGE_SD:
+      if (g.K == 2) {
+        if (!L || !R) return fail(STEREO_EINVAL, "SD needs L and R");
+        CU(launch_sd(g, L, R, b.Ls, b.Rs, s));
+      }
+      return STEREO_OK;
+    case STEREO_STAGE_PREP:
+      if (g.K == 1 && (!L || !R)) return fail(STEREO_EINVAL, "PREP with K=1 needs L and R");
+      CU(launch_prep(g, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, b, s));
+      return STEREO_OK;
+    case STEREO_STAGE_XPASS: CU(launch_xpass(g, h->plan, b, s)); return STEREO_OK;
+    case STEREO_STAGE_YPASS: CU(launch_ypass(g, h->plan, b, h->debug_ca, s)); return STEREO_OK;
+    case STEREO_STAGE_CCMED:
+      // in the full frame PREP resets the per-row records; standalone, reset them here
+      CU(cudaMemsetAsync(b.rowFirst, 0x7f, sizeof(int32_t) * g.Hs, s));
+      CU(cudaMemsetAsync(b.rowLast, 0xff, sizeof(int32_t) * g.Hs, s));
+      CU(launch_ccmed(g, b, s));
+      return STEREO_OK;
+    case STEREO_STAGE_FILL:
+      if (g.K == 1 && !disp_out) return fail(STEREO_EINVAL, "FILL with K=1 needs disp_out");
+      CU(launch_fill(g, b, g.K == 2 ? b.fill : disp_out, s));
+      return STEREO_OK;
+    case STEREO_STAGE_SU:
+      if (g.K == 2) {
+        if (!L || !disp_out) return fail(STEREO_EINVAL, "SU needs L and disp_out");
+        CU(launch_su(g, b.fill, L, disp_out, s));
+      }
+      return STEREO_OK;
+    default: return fail(STEREO_EINVAL, "unknown stage %d", stage_id);
+  }
+}
+
+int stereo_set_timing(stereo_t* h, int enable) {
+  if (!h) return fail(STEREO_EINVAL, "NULL handle");
+  for (size_t i = 0; i < h->pending.size(); ++i) {
+    cudaEventSynchronize(h->pending[i].ev[h->pending[i].n]);
+    for (int k = 0; k <= h->pending[i].n; ++k) h->pool.push_back(h->pending[i].ev[k]);
+  }
+  h->pending.clear();
+  for (double& v : h->acc_ms) v = 0;
+  h->acc_frames = 0;
+  h->timing = enable != 0;
+  return STEREO_OK;
+}
+
+int stereo_stage_times_ms(stereo_t* h, double* ms, int* nframes) {
+  if (!h || !ms) return fail(STEREO_EINVAL, "NULL argument");
+  for (size_t i = 0; i < h->pending.size(); ++i) {
+    int rc = drain_one(h, i);
+    if (rc) return rc;
+  }
+  h->pending.clear();
+  for (int i = 0; i < STEREO_STAGE_COUNT; ++i) ms[i] = h->acc_ms[i];
+  if (nframes) *nframes = h->acc_frames;
+  return STEREO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// stereo_internal.cuh — internal declarations shared by the kernels and the
+// host ABI of libstereo_b200.so (never exposed through include/stereo.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace stereo {
+
+constexpr int kInvalid = 255;  // INVALID disparity in u8 maps
+
+// Geometry and derived constants of one handle (all sizes in elements).
+struct Geom {
+  int W, H, D;      // original size and max disparity
+  int K, m_pool;    // scale factor, mean-pool radius
+  int Ws, Hs, Ds;   // scaled sizes
+  int Wp;           // row pitch (elements) of the CA_x volumes: Ws rounded up to 32
+  int w_x, w_y, delta, t_fill;
+  int f;            // fixed-point fraction bits
+  uint32_t border;  // 2^(f+1): the BORDER cost (reading R12b)
+  int8_t cdx[6], cdy[6];
+};
+
+// Device buffers owned by a handle.
+struct Buffers {
+  uint8_t* Ls = nullptr;   // scaled left  u8 [Hs][Ws] (K=2 only)
+  uint8_t* Rs = nullptr;   // scaled right u8 [Hs][Ws] (K=2 only)
+  uint16_t* pixL = nullptr;  // I | census << 8
+  uint16_t* pixR = nullptr;
+  uint32_t* armL = nullptr;  // m | n<<8 | M<<16 | N<<24
+  uint32_t* armR = nullptr;
+  uint32_t* caxL = nullptr;  // u32 [Ds][Hs][Wp]
+  uint32_t* caxR = nullptr;
+  uint64_t* caL = nullptr;   // debug only: u64 [Ds][Hs][Ws]
+  uint64_t* caR = nullptr;
+  uint8_t* DL = nullptr;
+  uint8_t* DR = nullptr;
+  uint8_t* masked = nullptr;
+  uint8_t* median = nullptr;
+  int32_t* rowFirst = nullptr;  // first valid x of the median map per row (or INT_MAX)
+  int32_t* rowLast = nullptr;   // last valid x (or -1)
+  float* fill = nullptr;        // f32 [Hs][Ws]
+  uint32_t* qad = nullptr;      // u32 [256]
+  uint32_t* qmc = nullptr;      // u32 [7]
+  // staging for stereo_compute_host
+  uint8_t* inL = nullptr;
+  uint8_t* inR = nullptr;
+  float* outF = nullptr;
+};
+
+// Launch configuration chosen at create time.
+struct Plan {
+  int xpass_C = 0;        // lane chunk (odd), Ws <= 32*C
+  int xpass_grid = 0;
+  int xpass_smem = 0;
+  int ypass_B = 0;        // output rows per tile
+  int ypass_T = 0;        // tile rows incl. halo
+  int ypass_smem = 0;
+  int ypass_nbuf = 2;
+};
+
+// Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch error.
+cudaError_t launch_sd(const Geom& g, const uint8_t* Lorg, const uint8_t* Rorg, uint8_t* Ls,
+                      uint8_t* Rs, cudaStream_t s);
+cudaError_t launch_prep(const Geom& g, const uint8_t* Ls, const uint8_t* Rs, Buffers& b,
+                        cudaStream_t s);
+cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s);
+cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
+                         cudaStream_t s);
+cudaError_t launch_ccmed(const Geom& g, Buffers& b, cudaStream_t s);
+cudaError_t launch_fill(const Geom& g, Buffers& b, float* out, cudaStream_t s);
+cudaError_t launch_su(const Geom& g, const float* fill, const uint8_t* Lorg, float* out,
+                      cudaStream_t s);
+
+// Plan helpers
+int xpass_chunk_for(int Ws);  // 0 if unsupported
+cudaError_t plan_kernels(const Geom& g, Plan& p, int device);
+
+}  // namespace stereo

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle's
+fixed mode, element by element, on seeded synthetic inputs.
+
+Integer stages (scaled images, census, arms, CA_x, CA, D^L, D^R, masked,
+median) must be bit-identical; the binary32 stages (fill, scale-up) must be
+bit-identical too (one correctly-rounded division / exact halvings, see
+DESIGN.md §2 R26, R30).  Tolerance vs the IEEE-double definition is covered
+by tests/test_oracle_pipeline.py::test_fixed_vs_double_tolerance plus
+test_ca_volume_tolerance_vs_double below.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2212_00488_b200 import abi, synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _run_gpu(L, R, D, st=None, **kw):
+    H, W = L.shape
+    own = st is None
+    if own:
+        st = abi.Stereo(W, H, D, **kw)
+    Lt = torch.from_numpy(np.ascontiguousarray(L)).to(DEV)
+    Rt = torch.from_numpy(np.ascontiguousarray(R)).to(DEV)
+    out = torch.full((H, W), float("nan"), dtype=torch.float32, device=DEV)
+    st.compute(Lt, Rt, out)
+    torch.cuda.synchronize()
+    res = {"out": out.cpu().numpy()}
+    i = st.info
+    pixL, pixR = st.download(abi.BUF_PIX_L), st.download(abi.BUF_PIX_R)
+    res["Ls"], res["cenL"] = abi.unpack_pix(pixL)
+    res["Rs"], res["cenR"] = abi.unpack_pix(pixR)
+    res["armL"] = abi.unpack_arms(st.download(abi.BUF_ARM_L))
+    res["armR"] = abi.unpack_arms(st.download(abi.BUF_ARM_R))
+    for name, b in (("DL", abi.BUF_DL), ("DR", abi.BUF_DR), ("masked", abi.BUF_MASKED),
+                    ("median", abi.BUF_MEDIAN)):
+        res[name] = st.download(b)
+    if kw.get("k_scale", 2) == 2:
+        res["fill"] = st.download(abi.BUF_FILL)
+    if i.Ds * i.Hs * i.cax_pitch * 4 <= 64 << 20:
+        res["caxL"] = st.download(abi.BUF_CAX_L)[:, :, :i.Ws]
+        res["caxR"] = st.download(abi.BUF_CAX_R)[:, :, :i.Ws]
+    if own:
+        st.close()
+    return res
+
+
+def _oracle_params(kw):
+    m = dict(kw)
+    census = m.pop("census", None)
+    if census is not None:
+        m["census"] = census
+    return oracle.params(**m)
+
+
+def _compare(L, R, D, kw, volumes=True):
+    stages = ["Ls", "Rs", "cenL", "cenR", "armL", "armR", "DL", "DR", "masked", "median", "out"]
+    if kw.get("k_scale", 2) == 2:
+        stages.append("fill")
+    if volumes:
+        stages += ["caxL", "caxR"]
+    ref = oracle.pipeline(L, R, D, _oracle_params(kw), "fixed", stages=tuple(stages))
+    got = _run_gpu(L, R, D, **kw)
+    for s in stages:
+        if s not in got:
+            continue
+        a, b = got[s], ref[s]
+        assert a.shape == b.shape, (s, a.shape, b.shape)
+        if a.dtype == np.float32:
+            same = a.view(np.uint32) == b.view(np.uint32)
+        else:
+            same = a == b
+        if not same.all():
+            idx = np.argwhere(~same)[:5]
+            raise AssertionError(f"stage {s}: {int((~same).sum())} mismatches, first at {idx.tolist()}: "
+                                 f"gpu={[a[tuple(i)] for i in idx]} oracle={[b[tuple(i)] for i in idx]}")
+    return got, ref
+
+
+# ---------------------------------------------------------------- tables
+def test_tables_identical_to_oracle():
+    for w_x in (0, 5, 21, 41, 141, 254):
+        st = abi.Stereo(64, 48, 16, w_x=w_x, k_scale=1)
+        qad, qmc, border = st.tables()
+        f = oracle.fixed_bits(w_x)
+        oqad, oqmc = oracle.fixed_tables(0.3, 2.3, f)
+        assert st.info.frac_bits == f
+        assert np.array_equal(qad, oqad) and np.array_equal(qmc, oqmc) and border == 2 ** (f + 1)
+        st.close()
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_c1_shift_pair_bit_exact():
+    L, R = synth.shift_pair(64, 48, 5, seed=0)
+    got, ref = _compare(L, R, 16, dict(k_scale=1))
+    assert (got["DL"][:, 26:] == 5).all()
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_random_small_instances(seed):
+    """SPEC acceptance 1: >=100 seeds, sizes up to 64x48, D<=16, random
+    delta / W / T / census pattern; every stage bit-exact."""
+    rng = np.random.default_rng(1000 + seed)
+    K = int(rng.choice([1, 2]))
+    W = int(rng.integers(1 * K, 65))
+    H = int(rng.integers(1 * K, 49))
+    W, H = max(W, K), max(H, K)
+    D = int(rng.integers(1, 17))
+    cand = [(dx, dy) for dx in range(-2, 3) for dy in range(-2, 3) if (dx, dy) != (0, 0)]
+    pat = [cand[i] for i in rng.choice(len(cand), 6, replace=False)] if rng.random() < 0.5 \
+        else list(oracle.DEFAULT_CENSUS)
+    kw = dict(k_scale=K, delta=int(rng.integers(1, 60)), w_x=int(rng.integers(0, 30)),
+              w_y=int(rng.integers(0, 40)), t_fill=int(rng.integers(0, 6)),
+              m_pool=int(rng.integers(0, 3)), census=pat)
+    kind = rng.integers(0, 3)
+    if kind == 0:
+        L, R = synth.random_pair(W, H, seed, levels=int(rng.choice([2, 8, 256])))
+    elif kind == 1:
+        L, R = synth.shift_pair(W, H, int(rng.integers(0, 6)), seed)
+    else:
+        L, R, _ = synth.scene(W, H, max(D, 2), seed)
+    _compare(L, R, D, kw)
+
+
+@pytest.mark.parametrize("W,H,D,K", [
+    (33, 17, 40, 1),      # D_s > W_s: every candidate beyond the image for many x
+    (737, 9, 64, 1),      # Ws > 736: next lane-chunk template, ragged tail
+    (100, 130, 1, 1),     # D = 1 (single candidate)
+    (1, 40, 5, 1),        # single column
+    (50, 1, 8, 1),        # single row
+    (131, 77, 33, 2),     # odd sizes with K = 2 (extra last column/row copies)
+    (2, 2, 3, 2),         # 1x1 scaled image
+    (290, 200, 100, 2),   # several xpass units, several ypass tiles, ragged strips
+])
+def test_edge_shapes(W, H, D, K):
+    L, R, _ = synth.scene(W, H, D, seed=W + H)
+    _compare(L, R, D, dict(k_scale=K))
+
+
+def test_c2_quarter_scene_bit_exact():
+    L, R, _ = synth.scene(450, 375, 64, seed=1)
+    _compare(L, R, 64, dict(k_scale=1))
+
+
+def test_c3_paper_workload_bit_exact():
+    """BASELINE config c3 in the launch configuration bench.py times."""
+    L, R, _ = synth.scene(1436, 992, 145, seed=0)
+    got, ref = _compare(L, R, 145, dict(), volumes=False)
+    assert got["out"].shape == (992, 1436)
+
+
+@pytest.mark.slow
+def test_c5_high_res_bit_exact():
+    L, R, _ = synth.scene(2872, 1984, 290, seed=0)
+    _compare(L, R, 290, dict(), volumes=False)
+
+
+def test_large_windows_next2():
+    """NEXT-2 window sizes (W_x=41, W_y=61) at K=1."""
+    L, R, _ = synth.scene(300, 200, 64, seed=5)
+    _compare(L, R, 64, dict(k_scale=1, w_x=41, w_y=61))
+
+
+# ---------------------------------------------------------------- CA volume
+def test_ca_volume_bit_exact_and_tolerance_vs_double():
+    L, R, _ = synth.scene(96, 72, 24, seed=4)
+    kw = dict(k_scale=1)
+    st = abi.Stereo(96, 72, 24, **kw)
+    st.set_debug(abi.DEBUG_CA, True)
+    _run_gpu(L, R, 24, st=st, **kw)
+    caL, caR = st.download(abi.BUF_CA_L), st.download(abi.BUF_CA_R)
+    f = st.info.frac_bits
+    st.close()
+    ref = oracle.pipeline(L, R, 24, oracle.params(k_scale=1), "fixed", stages=("caL", "caR"))
+    assert np.array_equal(caL, ref["caL"]) and np.array_equal(caR, ref["caR"])
+    dbl = oracle.pipeline(L, R, 24, oracle.params(k_scale=1), "double", stages=("caL_d", "caR_d"))
+    for a, b in ((caL, dbl["caL_d"]), (caR, dbl["caR_d"])):
+        q = a.astype(np.float64) / 2.0 ** f
+        rel = np.abs(q - b) / np.maximum(b, 1e-300)
+        rel[b == 0] = np.abs(q - b)[b == 0]
+        assert rel.max() <= 1e-5  # north_star tolerance
+
+
+def test_disparity_maps_vs_double_definition():
+    """<= 0.01% of D^L/D^R pixels may differ from the double-mode oracle, and
+    only where the two candidates' double costs tie within 1e-5 (north_star)."""
+    L, R, _ = synth.scene(450, 375, 64, seed=2)
+    got = _run_gpu(L, R, 64, k_scale=1)
+    dbl = oracle.pipeline(L, R, 64, oracle.params(k_scale=1), "double", stages=("DL", "DR"))
+    for m in ("DL", "DR"):
+        assert (got[m] != dbl[m]).mean() <= 1e-4
+
+
+# ---------------------------------------------------------------- stage isolation
+def test_stage_isolation_ypass_from_oracle_cax():
+    """Feed the oracle's CA_x and arms into the y pass alone."""
+    L, R, _ = synth.scene(200, 90, 40, seed=7)
+    p = oracle.params(k_scale=1)
+    ref = oracle.pipeline(L, R, 40, p, "fixed", stages=("caxL", "caxR", "armL", "armR", "DL", "DR"))
+    st = abi.Stereo(200, 90, 40, k_scale=1)
+    i = st.info
+    pad = lambda v: np.pad(v, ((0, 0), (0, 0), (0, i.cax_pitch - i.Ws)))
+    st.upload(abi.BUF_CAX_L, pad(ref["caxL"]))
+    st.upload(abi.BUF_CAX_R, pad(ref["caxR"]))
+    pack = lambda a: (a[0].astype(np.uint32) | a[1].astype(np.uint32) << 8 |
+                      a[2].astype(np.uint32) << 16 | a[3].astype(np.uint32) << 24)
+    st.upload(abi.BUF_ARM_L, pack(ref["armL"]))
+    st.upload(abi.BUF_ARM_R, pack(ref["armR"]))
+    st.run_stage(abi.STAGE_YPASS)
+    torch.cuda.synchronize()
+    assert np.array_equal(st.download(abi.BUF_DL), ref["DL"])
+    assert np.array_equal(st.download(abi.BUF_DR), ref["DR"])
+    st.close()
+
+
+def test_stage_isolation_post_from_oracle_maps():
+    L, R, _ = synth.scene(160, 100, 32, seed=8)
+    p = oracle.params()
+    ref = oracle.pipeline(L, R, 32, p, "fixed", stages=("DL", "DR", "masked", "median", "fill", "out", "Ls", "cenL"))
+    st = abi.Stereo(160, 100, 32)
+    st.upload(abi.BUF_DL, ref["DL"])
+    st.upload(abi.BUF_DR, ref["DR"])
+    st.upload(abi.BUF_PIX_L, ref["Ls"].astype(np.uint16) | (ref["cenL"].astype(np.uint16) << 8))
+    Lt = torch.from_numpy(L).to(DEV)
+    out = torch.zeros((100, 160), dtype=torch.float32, device=DEV)
+    st.run_stage(abi.STAGE_CCMED)
+    st.run_stage(abi.STAGE_FILL)
+    st.run_stage(abi.STAGE_SU, L=Lt, out=out)
+    torch.cuda.synchronize()
+    assert np.array_equal(st.download(abi.BUF_MASKED), ref["masked"])
+    assert np.array_equal(st.download(abi.BUF_MEDIAN), ref["median"])
+    assert np.array_equal(st.download(abi.BUF_FILL).view(np.uint32), ref["fill"].view(np.uint32))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref["out"].view(np.uint32))
+    st.close()
+
+
+def test_all_invalid_rows_rule_d():
+    """Rule (d): rows without any valid pixel (constructed via uploaded maps)."""
+    Ws, Hs = 40, 12
+    st = abi.Stereo(Ws, Hs, 8, k_scale=1)
+    rng = np.random.default_rng(3)
+    DL = rng.integers(0, 8, (Hs, Ws)).astype(np.uint8)
+    DR = np.full((Hs, Ws), 200, np.uint8)  # nothing cross-checks ...
+    for y in (4, 5, 9):                    # ... except rows 4, 5 and 9
+        DR[y] = 0
+        DL[y] = 0
+    L = rng.integers(0, 256, (Hs, Ws)).astype(np.uint8)
+    st.upload(abi.BUF_DL, DL)
+    st.upload(abi.BUF_DR, DR)
+    st.upload(abi.BUF_PIX_L, L.astype(np.uint16))
+    out = torch.zeros((Hs, Ws), dtype=torch.float32, device=DEV)
+    st.run_stage(abi.STAGE_CCMED)
+    st.run_stage(abi.STAGE_FILL, out=out)
+    torch.cuda.synchronize()
+    masked = oracle.cross_check(DL, DR)
+    med = oracle.median3x3(masked)
+    ref = oracle.fill_bilateral(med, L, 3)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    st.close()
+
+
+# ---------------------------------------------------------------- API behaviour
+def test_batch_host_and_repeat_determinism():
+    W, H, D = 200, 120, 48
+    frames = synth.stream(W, H, D, 7, seed=3)
+    st = abi.Stereo(W, H, D)
+    Lb = torch.from_numpy(np.stack([f[0] for f in frames])).to(DEV)
+    Rb = torch.from_numpy(np.stack([f[1] for f in frames])).to(DEV)
+    out = torch.zeros((7, H, W), dtype=torch.float32, device=DEV)
+    st.compute_batch(Lb, Rb, out, 7)
+    torch.cuda.synchronize()
+    outs = out.cpu().numpy()
+    for k, (L, R) in enumerate(frames):
+        ref = oracle.pipeline(L, R, D, oracle.params(), "fixed", stages=("out",))["out"]
+        assert np.array_equal(outs[k], ref)
+    # host-buffer (end-to-end) path
+    Lh = torch.from_numpy(frames[2][0]).pin_memory()
+    Rh = torch.from_numpy(frames[2][1]).pin_memory()
+    oh = torch.zeros((H, W), dtype=torch.float32).pin_memory()
+    st.compute_host(Lh, Rh, oh)
+    torch.cuda.synchronize()
+    assert np.array_equal(oh.numpy(), outs[2])
+    # a second stream gives the same bits
+    s2 = torch.cuda.Stream()
+    o2 = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    with torch.cuda.stream(s2):
+        st.compute(Lb[4], Rb[4], o2, stream=s2)
+    s2.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), outs[4])
+    st.close()
+
+
+def test_stage_timers():
+    W, H, D = 1436, 992, 145
+    L, R, _ = synth.scene(W, H, D, seed=0)
+    st = abi.Stereo(W, H, D)
+    Lt, Rt = torch.from_numpy(L).to(DEV), torch.from_numpy(R).to(DEV)
+    out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    st.set_timing(True)
+    for _ in range(3):
+        st.compute(Lt, Rt, out)
+    ms, n = st.stage_times_ms()
+    assert n == 3 and all(v > 0 for v in ms.values())
+    st.close()
