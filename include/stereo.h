@@ -166,16 +166,15 @@ int stereo_set_debug(stereo_t* h, int what, int enable);
 
 /* Run ONE stage on the handle's buffers (after stereo_debug_upload of its
  * inputs).  L, R: DEVICE u8 [H][W] originals (used by SD and, for K = 1, by
- * PREP); disp_out: DEVICE f32 [H][W] (written by SU; by FILL when K = 1).
- * Stage ids follow the paper's Table II taxonomy. */
+ * PREP); disp_out: DEVICE f32 [H][W] (written by POST).  Stage ids follow the
+ * paper's Table II taxonomy: SD | W^{LR}_+- and W^{*LR}_+- (PREP) |
+ * C+CA_x (XPASS) | CA (YPASS) | CC + Post + SU (POST). */
 enum {
   STEREO_STAGE_SD = 0,     /* Eq. 2 (K = 2 only; no-op for K = 1) */
-  STEREO_STAGE_PREP,       /* census + x/y arms: Table II W^{LR}_+-, W^{*LR}_+- */
-  STEREO_STAGE_XPASS,      /* C + CA_x */
-  STEREO_STAGE_YPASS,      /* CA + WTA */
-  STEREO_STAGE_CCMED,      /* CC + median */
-  STEREO_STAGE_FILL,       /* bilateral fill (Post) */
-  STEREO_STAGE_SU,         /* scale-up (K = 2 only) */
+  STEREO_STAGE_PREP,       /* census + x/y cross arms, both images */
+  STEREO_STAGE_XPASS,      /* C + CA_x, both bases */
+  STEREO_STAGE_YPASS,      /* CA + WTA, both bases */
+  STEREO_STAGE_POST,       /* cross-check + median + bilateral fill + scale-up */
   STEREO_STAGE_COUNT
 };
 int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,

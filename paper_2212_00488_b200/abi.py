@@ -25,9 +25,9 @@ STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, 
 
 (BUF_PIX_L, BUF_PIX_R, BUF_ARM_L, BUF_ARM_R, BUF_CAX_L, BUF_CAX_R, BUF_CA_L, BUF_CA_R,
  BUF_DL, BUF_DR, BUF_MASKED, BUF_MEDIAN, BUF_FILL) = range(13)
-(STAGE_SD, STAGE_PREP, STAGE_XPASS, STAGE_YPASS, STAGE_CCMED, STAGE_FILL, STAGE_SU) = range(7)
-STAGE_NAMES = ("SD", "PREP", "XPASS", "YPASS", "CCMED", "FILL", "SU")
-STAGE_COUNT = 7
+(STAGE_SD, STAGE_PREP, STAGE_XPASS, STAGE_YPASS, STAGE_POST) = range(5)
+STAGE_NAMES = ("SD", "PREP", "XPASS", "YPASS", "POST")
+STAGE_COUNT = 5
 DEBUG_CA = 1
 
 # every symbol include/stereo.h declares (checked by tests/test_abi.py)

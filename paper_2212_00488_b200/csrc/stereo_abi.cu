@@ -169,25 +169,19 @@ int enqueue_frame(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, c
   const uint8_t* Ls = L;
   const uint8_t* Rs = R;
   if (g.K == 2) {
-    CU(launch_sd(g, L, R, b.Ls, b.Rs, s));
+    CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, s));
     mark(STEREO_STAGE_SD);
     Ls = b.Ls;
     Rs = b.Rs;
   }
-  CU(launch_prep(g, Ls, Rs, b, s));
+  CU(launch_prep(g, h->plan, Ls, Rs, b, s));
   mark(STEREO_STAGE_PREP);
   CU(launch_xpass(g, h->plan, b, s));
   mark(STEREO_STAGE_XPASS);
   CU(launch_ypass(g, h->plan, b, h->debug_ca, s));
   mark(STEREO_STAGE_YPASS);
-  CU(launch_ccmed(g, b, s));
-  mark(STEREO_STAGE_CCMED);
-  CU(launch_fill(g, b, g.K == 2 ? b.fill : out, s));
-  mark(STEREO_STAGE_FILL);
-  if (g.K == 2) {
-    CU(launch_su(g, b.fill, L, out, s));
-    mark(STEREO_STAGE_SU);
-  }
+  CU(launch_post(g, h->plan, b, L, out, s));
+  mark(STEREO_STAGE_POST);
   if (h->timing) {
     h->pending.push_back(tf);
     if (h->pending.size() > 4096) {  // bound the event pool; the GPU is far behind anyway
@@ -290,6 +284,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
       {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
       {(void**)&b.rowFirst, (size_t)g.Hs * 4}, {(void**)&b.rowLast, (size_t)g.Hs * 4},
+      {(void**)&b.counter, 16},
       {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
   };
   for (auto& a : as) {
@@ -301,9 +296,10 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       return rc;
     }
   }
-  e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
+  e = cudaMemset(b.counter, 0, 16);
+  if (e == cudaSuccess) e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(b.qmc, h->qmc_h, sizeof h->qmc_h, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = plan_kernels(g, h->plan, h->device);
+  if (e == cudaSuccess) e = plan_kernels(g, h->plan, b, h->device);
   if (e != cudaSuccess) {
     stereo_destroy(h);
     return fail(STEREO_ECUDA, "setup: %s", cudaGetErrorString(e));
@@ -378,7 +374,7 @@ int stereo_get_info(const stereo_t* h, stereo_info* info) {
   if (g.K == 2) tot += 2 * n;
   info->device_bytes = tot;
   info->cax_bytes = vol * 4;
-  info->launches_per_frame = g.K == 2 ? 7 : 5;
+  info->launches_per_frame = g.K == 2 ? 5 : 4;
   info->ypass_block_rows = h->plan.ypass_B;
   info->cax_pitch = g.Wp;
   return STEREO_OK;
@@ -434,30 +430,18 @@ int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t*
     case STEREO_STAGE_SD:
       if (g.K == 2) {
         if (!L || !R) return fail(STEREO_EINVAL, "SD needs L and R");
-        CU(launch_sd(g, L, R, b.Ls, b.Rs, s));
+        CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, s));
       }
       return STEREO_OK;
     case STEREO_STAGE_PREP:
       if (g.K == 1 && (!L || !R)) return fail(STEREO_EINVAL, "PREP with K=1 needs L and R");
-      CU(launch_prep(g, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, b, s));
+      CU(launch_prep(g, h->plan, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, b, s));
       return STEREO_OK;
     case STEREO_STAGE_XPASS: CU(launch_xpass(g, h->plan, b, s)); return STEREO_OK;
     case STEREO_STAGE_YPASS: CU(launch_ypass(g, h->plan, b, h->debug_ca, s)); return STEREO_OK;
-    case STEREO_STAGE_CCMED:
-      // in the full frame PREP resets the per-row records; standalone, reset them here
-      CU(cudaMemsetAsync(b.rowFirst, 0x7f, sizeof(int32_t) * g.Hs, s));
-      CU(cudaMemsetAsync(b.rowLast, 0xff, sizeof(int32_t) * g.Hs, s));
-      CU(launch_ccmed(g, b, s));
-      return STEREO_OK;
-    case STEREO_STAGE_FILL:
-      if (g.K == 1 && !disp_out) return fail(STEREO_EINVAL, "FILL with K=1 needs disp_out");
-      CU(launch_fill(g, b, g.K == 2 ? b.fill : disp_out, s));
-      return STEREO_OK;
-    case STEREO_STAGE_SU:
-      if (g.K == 2) {
-        if (!L || !disp_out) return fail(STEREO_EINVAL, "SU needs L and disp_out");
-        CU(launch_su(g, b.fill, L, disp_out, s));
-      }
+    case STEREO_STAGE_POST:
+      if (!disp_out || (g.K == 2 && !L)) return fail(STEREO_EINVAL, "POST needs disp_out (and L when K=2)");
+      CU(launch_post(g, h->plan, b, L, disp_out, s));
       return STEREO_OK;
     default: return fail(STEREO_EINVAL, "unknown stage %d", stage_id);
   }

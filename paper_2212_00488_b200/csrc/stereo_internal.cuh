@@ -1,6 +1,7 @@
 // stereo_internal.cuh — internal declarations shared by the kernels and the
 // host ABI of libstereo_b200.so (never exposed through include/stereo.h).
 #pragma once
+#include <cuda.h>  // CUtensorMap (the driver entry point is resolved at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,8 +23,8 @@ struct Geom {
 
 // Device buffers owned by a handle.
 struct Buffers {
-  uint8_t* Ls = nullptr;   // scaled left  u8 [Hs][Ws] (K=2 only)
-  uint8_t* Rs = nullptr;   // scaled right u8 [Hs][Ws] (K=2 only)
+  uint8_t* Ls = nullptr;     // scaled left  u8 [Hs][Ws] (K=2 only)
+  uint8_t* Rs = nullptr;     // scaled right u8 [Hs][Ws] (K=2 only)
   uint16_t* pixL = nullptr;  // I | census << 8
   uint16_t* pixR = nullptr;
   uint32_t* armL = nullptr;  // m | n<<8 | M<<16 | N<<24
@@ -36,8 +37,9 @@ struct Buffers {
   uint8_t* DR = nullptr;
   uint8_t* masked = nullptr;
   uint8_t* median = nullptr;
-  int32_t* rowFirst = nullptr;  // first valid x of the median map per row (or INT_MAX)
+  int32_t* rowFirst = nullptr;  // first valid x of the median map per row (or -1)
   int32_t* rowLast = nullptr;   // last valid x (or -1)
+  unsigned* counter = nullptr;  // POST last-block counter (self-resetting)
   float* fill = nullptr;        // f32 [Hs][Ws]
   uint32_t* qad = nullptr;      // u32 [256]
   uint32_t* qmc = nullptr;      // u32 [7]
@@ -49,30 +51,33 @@ struct Buffers {
 
 // Launch configuration chosen at create time.
 struct Plan {
-  int xpass_C = 0;        // lane chunk (odd), Ws <= 32*C
+  int xpass_C = 0;  // lane chunk (odd), Ws <= 32*C
   int xpass_grid = 0;
   int xpass_smem = 0;
-  int ypass_B = 0;        // output rows per tile
-  int ypass_T = 0;        // tile rows incl. halo
+  int xpass_PL = 0;  // per-warp prefix buffer length
+  int ypass_B = 0;   // output rows per tile (<= 8*kYRPT)
+  int ypass_nb = 0;  // tiles per column strip
+  int ypass_SEG = 0; // tile rows per warp; TMA box height = 8*SEG
   int ypass_smem = 0;
-  int ypass_nbuf = 2;
+  CUtensorMap tmL, tmR;  // 3-D maps over the CA_x volumes {Wp, Hs, Ds}
+  int post_smem = 0;
+  int sd_smem = 0;
+  int prep_smem = 0;
 };
 
 // Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch error.
-cudaError_t launch_sd(const Geom& g, const uint8_t* Lorg, const uint8_t* Rorg, uint8_t* Ls,
-                      uint8_t* Rs, cudaStream_t s);
-cudaError_t launch_prep(const Geom& g, const uint8_t* Ls, const uint8_t* Rs, Buffers& b,
-                        cudaStream_t s);
+cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const uint8_t* Rorg,
+                      uint8_t* Ls, uint8_t* Rs, cudaStream_t s);
+cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
+                        Buffers& b, cudaStream_t s);
 cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s);
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
                          cudaStream_t s);
-cudaError_t launch_ccmed(const Geom& g, Buffers& b, cudaStream_t s);
-cudaError_t launch_fill(const Geom& g, Buffers& b, float* out, cudaStream_t s);
-cudaError_t launch_su(const Geom& g, const float* fill, const uint8_t* Lorg, float* out,
-                      cudaStream_t s);
+cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
+                        float* out, cudaStream_t s);
 
 // Plan helpers
 int xpass_chunk_for(int Ws);  // 0 if unsupported
-cudaError_t plan_kernels(const Geom& g, Plan& p, int device);
+cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device);
 
 }  // namespace stereo

@@ -1,10 +1,15 @@
-// stereo_kernels.cu — sm_100a kernels of the stereo hot path (v1).
+// stereo_kernels.cu — sm_100a kernels of the stereo hot path.
 //
-// One kernel per Table II stage.  Every kernel cites the passage it
-// implements; DESIGN.md §4 gives each one's data layout, roofline and
-// algorithmic bytes.  Integer/fixed-point throughout up to WTA (bit-exact with
-// the oracle's fixed mode); binary32 with explicit round-to-nearest intrinsics
-// (no FMA contraction) for the fill and scale-up.
+// Five kernels per frame, one per Table II group:
+//   sd_kernel    SD                      (Eq. 2)
+//   prep_kernel  W^{LR}_+- and W^{*LR}_+- (census + cross arms)
+//   xpass_kernel C + CA_x                (Eqs. 3-7, both bases from one prefix row)
+//   ypass_kernel CA + WTA                (Eqs. 8-9; TMA tile loads)
+//   post_kernel  CC + Post + SU          (Eq. 10, median, Eq. 11 fill, Step8)
+// Every kernel cites the passage it implements; DESIGN.md §4 gives each one's
+// layout, roofline and algorithmic bytes.  Integer / fixed point up to WTA
+// (bit-exact with the oracle's fixed mode); binary32 with explicit
+// round-to-nearest intrinsics (no FMA contraction) for the fill and scale-up.
 #include <climits>
 #include <cstdio>
 
@@ -15,124 +20,174 @@ namespace stereo {
 namespace {
 constexpr unsigned kFull = 0xffffffffu;
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 }  // namespace
 
 // ============================================================================
 // SD — Eq. 2, Step1: L(x,y) = mean of the (2m+1)^2
-// block of L_org around (Kx, Ky), border-clamped, rounded half up:
-// floor((2*sum + n) / (2n)), n = (2m+1)^2.  K = 2 only (K = 1: no scaling).
-// HBM-bound: reads 2*W*H bytes, writes 2*Ws*Hs bytes.
+// block of L_org around (2x, 2y), border-clamped, rounded half up:
+// floor((2*sum + n) / (2n)), n = (2m+1)^2.  One CTA per output row and image:
+// the 2m+1 source rows are staged in shared memory with 4-byte loads.
 // ============================================================================
-__global__ void __launch_bounds__(128) sd_kernel(const uint8_t* __restrict__ Lorg,
+template <int M>
+__global__ void __launch_bounds__(256) sd_kernel(const uint8_t* __restrict__ Lorg,
                                                  const uint8_t* __restrict__ Rorg,
                                                  uint8_t* __restrict__ Ls,
                                                  uint8_t* __restrict__ Rs, int W, int H,
-                                                 int Ws, int Hs, int m) {
-  const uint8_t* src = blockIdx.z ? Rorg : Lorg;
-  uint8_t* dst = blockIdx.z ? Rs : Ls;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  if (x >= Ws) return;
-  const int n = (2 * m + 1) * (2 * m + 1);
-  int sum = 0;
-  for (int j = -m; j <= m; ++j) {
-    const uint8_t* row = src + (size_t)clampi(2 * y + j, 0, H - 1) * W;
-    for (int i = -m; i <= m; ++i) sum += __ldg(row + clampi(2 * x + i, 0, W - 1));
+                                                 int Ws) {
+  extern __shared__ uint32_t sdm32[];
+  uint8_t* sdm = reinterpret_cast<uint8_t*>(sdm32);
+  constexpr int NR = 2 * M + 1, N = NR * NR;
+  const uint8_t* src = blockIdx.y ? Rorg : Lorg;
+  uint8_t* dst = blockIdx.y ? Rs : Ls;
+  const int y = blockIdx.x;
+  const int Wq = (W + 3) & ~3;
+  const bool vec = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 3) == 0);
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const uint8_t* row = src + (size_t)clampi(2 * y + j - M, 0, H - 1) * W;
+    if (vec) {
+      const uint32_t* r4 = reinterpret_cast<const uint32_t*>(row);
+      for (int i = threadIdx.x; i < (W >> 2); i += blockDim.x) sdm32[j * (Wq >> 2) + i] = __ldg(r4 + i);
+    } else {
+      for (int i = threadIdx.x; i < W; i += blockDim.x) sdm[j * Wq + i] = __ldg(row + i);
+    }
   }
-  dst[(size_t)y * Ws + x] = (uint8_t)((2 * sum + n) / (2 * n));
+  __syncthreads();
+  for (int x = threadIdx.x; x < Ws; x += blockDim.x) {
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int i = -M; i <= M; ++i) sum += sdm[j * Wq + clampi(2 * x + i, 0, W - 1)];
+    dst[(size_t)y * Ws + x] = (uint8_t)((2 * sum + N) / (2 * N));
+  }
 }
 
-cudaError_t launch_sd(const Geom& g, const uint8_t* Lorg, const uint8_t* Rorg, uint8_t* Ls,
-                      uint8_t* Rs, cudaStream_t s) {
-  dim3 grid((g.Ws + 127) / 128, g.Hs, 2);
-  sd_kernel<<<grid, 128, 0, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws, g.Hs, g.m_pool);
+cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const uint8_t* Rorg,
+                      uint8_t* Ls, uint8_t* Rs, cudaStream_t s) {
+  dim3 grid(g.Hs, 2);
+  switch (g.m_pool) {
+    case 0: sd_kernel<0><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
+    case 1: sd_kernel<1><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
+    case 2: sd_kernel<2><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
+    default: sd_kernel<3><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
+  }
   return cudaGetLastError();
 }
 
 // ============================================================================
 // PREP — mini-census (Fig. 3; pattern is a parameter, reading R8)
 // and the four cross arms (Steps 2 and 4)
-// of both scaled images in one pass.  A 32x8 pixel tile is staged in shared
-// memory as two strips: a vertical one (rows +-max(w_y,2), cols +-2) for the
-// census and the y arms, a horizontal one (rows +-2, cols +-max(w_x,2)) for
-// the x arms.  Coordinates are clamped on load (census border rule R11); arm
-// scans stop at the real image border (R16) and at the first |dI| >= delta.
-// Output: pix = I | code << 8 (u16), arm = m | n<<8 | M<<16 | N<<24 (u32).
-// Also resets the per-row first/last-valid records used by FILL rule (d).
+// of both scaled images.  A 32x8 pixel tile is staged in shared memory as a
+// horizontal strip (rows +-2, cols +-max(w_x,2)) for the census and the x
+// arms and a TRANSPOSED vertical strip (cols +-2, rows +-max(w_y,2)) for the
+// y arms, so that both arm scans read contiguous bytes: 4 neighbours are
+// tested per step with byte-SIMD (|dI| via vabsdiffu4, >= delta via
+// vcmpgeu4), the run ends at the first dissimilar byte (ffs/clz).
+// Coordinates are clamped on load (census border rule R11); arm scans stop at
+// the real image border (R16).  Output: pix = I | code << 8 (u16),
+// arm = m | n<<8 | M<<16 | N<<24 (u32).
 // ============================================================================
 struct PrepArgs {
-  const uint8_t* img[2];
-  uint16_t* pix[2];
-  uint32_t* arm[2];
-  int32_t* rowFirst;
-  int32_t* rowLast;
+  const uint8_t* img0;
+  const uint8_t* img1;
+  uint16_t* pix0;
+  uint16_t* pix1;
+  uint32_t* arm0;
+  uint32_t* arm1;
   int Ws, Hs, w_x, w_y, delta;
+  int HX, HY, BWp, AHp;  // halos and padded strip pitches
   int8_t cdx[6], cdy[6];
 };
 
+__device__ __forceinline__ uint32_t ld4u(const uint8_t* p) {  // 4 bytes at any alignment
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  return __funnelshift_r(q[0], q[1], (uint32_t)(a & 3) * 8u);
+}
+// similar run going forward: p[0] is the first neighbour
+__device__ __forceinline__ int run_fwd(const uint8_t* p, int lim, uint32_t c4, uint32_t d4) {
+  for (int n = 0; n < lim; n += 4) {
+    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(p + n), c4), d4);
+    if (ge) return min(n + ((__ffs(ge) - 1) >> 3), lim);
+  }
+  return lim;
+}
+// similar run going backward: p[-1] is the first neighbour
+__device__ __forceinline__ int run_bwd(const uint8_t* p, int lim, uint32_t c4, uint32_t d4) {
+  for (int n = 0; n < lim; n += 4) {
+    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(p - n - 4), c4), d4);
+    if (ge) return min(n + (__clz(ge) >> 3), lim);
+  }
+  return lim;
+}
+
 __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
-  extern __shared__ uint8_t psm[];
-  const int hy = max(a.w_y, 2), hx = max(a.w_x, 2);
-  const int AW = 36, AH = 8 + 2 * hy;
-  const int BW = 32 + 2 * hx, BH = 12;
-  uint8_t* sA = psm;
-  uint8_t* sB = psm + AW * AH;
-  const uint8_t* img = blockIdx.z ? a.img[1] : a.img[0];
+  extern __shared__ uint32_t psm32[];
+  uint8_t* sB = reinterpret_cast<uint8_t*>(psm32);  // [12][BWp]  horizontal strip
+  uint8_t* sV = sB + 12 * a.BWp;                      // [36][AHp]  vertical strip, transposed
+  const uint8_t* img = blockIdx.z ? a.img1 : a.img0;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int i = tid; i < AW * AH; i += 256) {
-    int r = i / AW, c = i % AW;
-    sA[i] = __ldg(img + (size_t)clampi(y0 - hy + r, 0, a.Hs - 1) * a.Ws +
-                  clampi(x0 - 2 + c, 0, a.Ws - 1));
-  }
-  for (int i = tid; i < BW * BH; i += 256) {
-    int r = i / BW, c = i % BW;
+  const int HX = a.HX, HY = a.HY, BWp = a.BWp, AHp = a.AHp;
+  for (int i = tid; i < 12 * BWp; i += 256) {
+    const int r = i / BWp, c = i - r * BWp;
     sB[i] = __ldg(img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws +
-                  clampi(x0 - hx + c, 0, a.Ws - 1));
+                  clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
+  }
+  for (int i = tid; i < 36 * AHp; i += 256) {
+    const int r = i / 36, c = i - r * 36;  // consecutive threads: consecutive columns
+    sV[c * AHp + r] = __ldg(img + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws +
+                            clampi(x0 - 2 + c, 0, a.Ws - 1));
   }
   __syncthreads();
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int x = x0 + tx, y = y0 + ty;
-  if (blockIdx.x == 0 && blockIdx.z == 0 && tx == 0 && y < a.Hs) {
-    a.rowFirst[y] = INT_MAX;
-    a.rowLast[y] = -1;
-  }
   if (x >= a.Ws || y >= a.Hs) return;
-  const int c = sA[(ty + hy) * AW + tx + 2];
+  const uint8_t* ctr = sB + (ty + 2) * BWp + tx + HX + 8;
+  const int c = *ctr;
   int code = 0;
 #pragma unroll
-  for (int i = 0; i < 6; ++i)
-    code |= (sA[(ty + hy + a.cdy[i]) * AW + tx + 2 + a.cdx[i]] < c) << i;
-  const uint8_t* rowB = sB + (ty + 2) * BW + tx + hx;
-  int n = 0;
-  while (n < a.w_x && x + n + 1 <= a.Ws - 1 && abs((int)rowB[n + 1] - c) < a.delta) ++n;
-  int m = 0;
-  while (m < a.w_x && x - m - 1 >= 0 && abs((int)rowB[-m - 1] - c) < a.delta) ++m;
-  const uint8_t* colA = sA + (ty + hy) * AW + tx + 2;
-  int N = 0;
-  while (N < a.w_y && y + N + 1 <= a.Hs - 1 && abs((int)colA[(N + 1) * AW] - c) < a.delta) ++N;
-  int M = 0;
-  while (M < a.w_y && y - M - 1 >= 0 && abs((int)colA[-(M + 1) * AW] - c) < a.delta) ++M;
+  for (int i = 0; i < 6; ++i) code |= (ctr[a.cdy[i] * BWp + a.cdx[i]] < c) << i;
+  int n, m, N, M;
+  if (a.delta > 255) {  // |dI| <= 255 < delta: every neighbour is similar
+    n = min(a.w_x, a.Ws - 1 - x); m = min(a.w_x, x);
+    N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
+  } else {
+    const uint32_t c4 = (uint32_t)c * 0x01010101u, d4 = (uint32_t)a.delta * 0x01010101u;
+    n = run_fwd(ctr + 1, min(a.w_x, a.Ws - 1 - x), c4, d4);
+    m = run_bwd(ctr, min(a.w_x, x), c4, d4);
+    const uint8_t* col = sV + (tx + 2) * AHp + ty + HY + 8;
+    N = run_fwd(col + 1, min(a.w_y, a.Hs - 1 - y), c4, d4);
+    M = run_bwd(col, min(a.w_y, y), c4, d4);
+  }
   const size_t o = (size_t)y * a.Ws + x;
-  uint16_t* pix = blockIdx.z ? a.pix[1] : a.pix[0];
-  uint32_t* armo = blockIdx.z ? a.arm[1] : a.arm[0];
-  pix[o] = (uint16_t)(c | (code << 8));
-  armo[o] = (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
+  (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
+  (blockIdx.z ? a.arm1 : a.arm0)[o] =
+      (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
 }
 
-cudaError_t launch_prep(const Geom& g, const uint8_t* Ls, const uint8_t* Rs, Buffers& b,
-                        cudaStream_t s) {
+static void prep_geometry(const Geom& g, int& HX, int& HY, int& BWp, int& AHp) {
+  HX = g.w_x > 2 ? g.w_x : 2;
+  HY = g.w_y > 2 ? g.w_y : 2;
+  BWp = (32 + 2 * HX + 16 + 15) & ~15;
+  AHp = (8 + 2 * HY + 16 + 15) & ~15;
+}
+
+cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
+                        Buffers& b, cudaStream_t s) {
   PrepArgs a;
-  a.img[0] = Ls; a.img[1] = Rs;
-  a.pix[0] = b.pixL; a.pix[1] = b.pixR;
-  a.arm[0] = b.armL; a.arm[1] = b.armR;
-  a.rowFirst = b.rowFirst; a.rowLast = b.rowLast;
+  a.img0 = Ls; a.img1 = Rs;
+  a.pix0 = b.pixL; a.pix1 = b.pixR;
+  a.arm0 = b.armL; a.arm1 = b.armR;
   a.Ws = g.Ws; a.Hs = g.Hs; a.w_x = g.w_x; a.w_y = g.w_y; a.delta = g.delta;
+  prep_geometry(g, a.HX, a.HY, a.BWp, a.AHp);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
-  const int hy = g.w_y > 2 ? g.w_y : 2, hx = g.w_x > 2 ? g.w_x : 2;
-  const size_t smem = 36 * (8 + 2 * hy) + 12 * (32 + 2 * hx);
   dim3 grid((g.Ws + 31) / 32, (g.Hs + 7) / 8, 2);
-  prep_kernel<<<grid, dim3(32, 8), smem, s>>>(a);
+  prep_kernel<<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -142,18 +197,18 @@ cudaError_t launch_prep(const Geom& g, const uint8_t* Ls, const uint8_t* Rs, Buf
 // (Eq. 6): C^R(x,d) = C^L(x+d,d), so ONE exclusive prefix row
 //   P[k] = sum_{x'<k} Q(x',d)   (u32, modular: window sums < 2^32 are exact)
 // gives  CA^L_x(x,d) = P[x+n_L+1] - P[x-m_L]
-//        CA^R_x(x,d) = P[x+d+n_R+1] - P[x+d-m_R]   (P extended by BORDER
-//                                                    beyond Ws)
-// replacing the paper's O(W_x) direct sums by O(1) differences.
+//        CA^R_x(x,d) = P[x+d+n_R+1] - P[x+d-m_R]
+// with P extended by BORDER = 2^(f+1) per column beyond Ws, replacing
+// the paper's O(W_x) direct sums by O(1) differences.
 // Work unit = (row y, 16 consecutive d); each warp owns one d at a time:
 //   phase A: lane l scans its contiguous chunk [lC, lC+C) (C odd -> shared
 //            loads at stride C are bank-conflict free); costs from the fixed
 //            tables Q_AD[|dI|] and Q_MC[cL ^ cR] (popc folded into a 64-entry
-//            table), both replicated per bank (index*32 + lane);
+//            table), both replicated per bank (index*32 + lane); branch-free
+//            BORDER select for x < d;
 //   warp scan of the 32 lane totals (shuffles) -> P into shared memory;
 //   phase C: lanes interleaved over x -> two coalesced 128-B stores per warp.
 // Output layout: u32 [Ds][Hs][Wp] (Wp = Ws rounded up to 32).
-// Bound: HBM writes (8 B per (x,y,d)) vs shared-memory wavefronts.
 // ============================================================================
 struct XArgs {
   const uint16_t* pixL;
@@ -164,7 +219,7 @@ struct XArgs {
   const uint32_t* qmc;
   uint32_t* caxL;
   uint32_t* caxR;
-  int Ws, Hs, Ds, Wp;
+  int Ws, Hs, Ds, Wp, PL, ext;
   uint32_t border;
 };
 
@@ -172,7 +227,7 @@ constexpr int kXWarps = 8;
 constexpr int kXDPerUnit = 16;
 
 template <int C>
-__global__ void __launch_bounds__(kXWarps * 32) xpass_kernel(XArgs a) {
+__global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
   extern __shared__ uint32_t xsm[];
   uint32_t* sQAD = xsm;              // [256][32]
   uint32_t* sQMC = sQAD + 256 * 32;  // [64][32], indexed by cL ^ cR
@@ -180,7 +235,7 @@ __global__ void __launch_bounds__(kXWarps * 32) xpass_kernel(XArgs a) {
   uint32_t* sR = sL + 32 * C;        // [32C] pixR row
   uint32_t* sA = sR + 32 * C;        // [32C] mL | nL<<8 | mR<<16 | nR<<24
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* P = sA + 32 * C + warp * (32 * C + 1);  // [32C+1] exclusive prefix
+  uint32_t* P = sA + 32 * C + warp * a.PL;  // [PL] exclusive prefix (+ BORDER extension)
 
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sQAD[i] = __ldg(a.qad + (i >> 5));
   for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) sQMC[i] = __ldg(a.qmc + __popc(i >> 5));
@@ -190,17 +245,17 @@ __global__ void __launch_bounds__(kXWarps * 32) xpass_kernel(XArgs a) {
   const int Ws = a.Ws;
   const uint32_t border = a.border;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const int y = u / nch, d0 = (u % nch) * kXDPerUnit;
+    const int y = u / nch, d0 = (u - y * nch) * kXDPerUnit;
     __syncthreads();  // previous unit finished with the row buffers
     for (int x = threadIdx.x; x < 32 * C; x += blockDim.x) {
+      uint32_t l = 0, r = 0, ar = 0;
       if (x < Ws) {
         const size_t o = (size_t)y * Ws + x;
-        sL[x] = __ldg(a.pixL + o);
-        sR[x] = __ldg(a.pixR + o);
-        sA[x] = (__ldg(a.armL + o) & 0xffffu) | (__ldg(a.armR + o) << 16);
-      } else {
-        sL[x] = 0; sR[x] = 0; sA[x] = 0;
+        l = __ldg(a.pixL + o);
+        r = __ldg(a.pixR + o);
+        ar = (__ldg(a.armL + o) & 0xffffu) | (__ldg(a.armR + o) << 16);
       }
+      sL[x] = l; sR[x] = r; sA[x] = ar;
     }
     __syncthreads();
 #pragma unroll 1
@@ -208,18 +263,18 @@ __global__ void __launch_bounds__(kXWarps * 32) xpass_kernel(XArgs a) {
       const int d = d0 + j * kXWarps + warp;
       if (d >= a.Ds) break;
       // ---- phase A: costs of the lane's chunk + local inclusive prefix
+      const uint32_t* Lr = sL + lane * C;
+      const uint32_t* Rr = sR + lane * C - d;  // may point before sR: those lanes take BORDER
+      const int nb = d - lane * C;             // elements k < nb have x - d < 0
       uint32_t pref[C];
       uint32_t run = 0;
 #pragma unroll
       for (int k = 0; k < C; ++k) {
-        const int x = lane * C + k;
-        uint32_t q = border;  // x - d < 0: out of the right image (reading R12b)
-        if (x >= d) {
-          const uint32_t pl = sL[x], pr = sR[x - d];
-          const int ad = abs((int)(pl & 255u) - (int)(pr & 255u));
-          const uint32_t hx = ((pl ^ pr) >> 8) & 63u;
-          q = sQAD[ad * 32 + lane] + sQMC[hx * 32 + lane];
-        }
+        const uint32_t pl = Lr[k], pr = Rr[k];
+        const uint32_t ad = __vabsdiffu4(pl, pr) & 255u;
+        const uint32_t hx = ((pl ^ pr) >> 8) & 63u;
+        uint32_t q = sQAD[(ad << 5) | lane] + sQMC[(hx << 5) | lane];
+        q = (k < nb) ? border : q;  // reading R12b: out of the right image
         run += q;
         pref[k] = run;
       }
@@ -230,26 +285,27 @@ __global__ void __launch_bounds__(kXWarps * 32) xpass_kernel(XArgs a) {
         if (lane >= o) incl += t;
       }
       const uint32_t off = incl - run;
+      uint32_t* Pl = P + lane * C + 1;
 #pragma unroll
-      for (int k = 0; k < C; ++k) P[lane * C + k + 1] = pref[k] + off;
+      for (int k = 0; k < C; ++k) Pl[k] = pref[k] + off;
       if (lane == 0) P[0] = 0;
       __syncwarp();
-      // ---- phase C: window differences, coalesced stores
       const uint32_t PW = P[Ws];
+      for (int e = lane; e < a.ext; e += 32) P[Ws + 1 + e] = PW + (uint32_t)(e + 1) * border;
+      __syncwarp();
+      // ---- phase C: window differences, coalesced stores
       uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp;
       uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp;
-#pragma unroll 4
+      const uint32_t* Pd = P + d;
+#pragma unroll
       for (int i = 0; i < C; ++i) {
         const int x = lane + 32 * i;
+        const uint32_t ar = sA[x];
+        const uint32_t caL = P[x + ((ar >> 8) & 255u) + 1] - P[x - (int)(ar & 255u)];
+        const uint32_t caR = Pd[x + (ar >> 24) + 1] - Pd[x - (int)((ar >> 16) & 255u)];
         if (x < Ws) {
-          const uint32_t ar = sA[x];
-          const int mL = ar & 255u, nL = (ar >> 8) & 255u, mR = (ar >> 16) & 255u, nR = ar >> 24;
-          const uint32_t caL = P[x + nL + 1] - P[x - mL];
-          const int hi = x + d + nR + 1, lo = x + d - mR;
-          const uint32_t Phi = hi <= Ws ? P[hi] : PW + (uint32_t)(hi - Ws) * border;
-          const uint32_t Plo = lo <= Ws ? P[lo] : PW + (uint32_t)(lo - Ws) * border;
           outL[x] = caL;
-          outR[x] = Phi - Plo;
+          outR[x] = caR;
         }
       }
       __syncwarp();
@@ -264,14 +320,10 @@ int xpass_chunk_for(int Ws) {
   return 0;
 }
 
-static size_t xpass_smem_bytes(int C) {
-  return sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + 3 * 32 * C + kXWarps * (32 * C + 1));
-}
-
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.pixL, b.pixR, b.armL, b.armR, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, g.border};
+          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x, g.border};
   xpass_kernel<C><<<p.xpass_grid, kXWarps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -288,16 +340,16 @@ static int occ_xpass_c(int smem) {
   return n;
 }
 
-#define XPASS_DISPATCH(C_, EXPR) \
-  switch (C_) {                  \
-    case 3: { constexpr int CC = 3; EXPR; } break;   \
-    case 7: { constexpr int CC = 7; EXPR; } break;   \
-    case 15: { constexpr int CC = 15; EXPR; } break; \
-    case 23: { constexpr int CC = 23; EXPR; } break; \
-    case 31: { constexpr int CC = 31; EXPR; } break; \
-    case 47: { constexpr int CC = 47; EXPR; } break; \
-    case 63: { constexpr int CC = 63; EXPR; } break; \
-    default: break;              \
+#define XPASS_DISPATCH(C_, EXPR)                        \
+  switch (C_) {                                         \
+    case 3: { constexpr int CC = 3; EXPR; } break;      \
+    case 7: { constexpr int CC = 7; EXPR; } break;      \
+    case 15: { constexpr int CC = 15; EXPR; } break;    \
+    case 23: { constexpr int CC = 23; EXPR; } break;    \
+    case 31: { constexpr int CC = 31; EXPR; } break;    \
+    case 47: { constexpr int CC = 47; EXPR; } break;    \
+    case 63: { constexpr int CC = 63; EXPR; } break;    \
+    default: break;                                     \
   }
 
 cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
@@ -308,190 +360,346 @@ cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t 
 
 // ============================================================================
 // YPASS — y aggregation (Eq. 8) + WTA (Eq. 9) for one
-// base, Step5.  CTA = 32-column strip x B output rows; loops over
-// d.  Per d the CTA loads the tile rows [y0-w_y, y0+B+w_y) of CA_x (coalesced
-// 128-B rows), builds the exact u64 column prefix E (each warp a row segment
-// serially in registers, segment offsets via shared memory), then every
-// output pixel takes CA = E[y+N+1] - E[y-M] (O(1) instead of O(W_y)) and keeps
-// the running minimum with the paper's strict "<": ties keep the
-// smallest d.  Double-buffered prefix -> two barriers per d.
+// base, Step5.  CTA = 32-column strip x B output rows, looping over
+// d.  Per d a TMA 3-D box {32 columns, T = 8*SEG rows, 1 disparity} of the
+// CA_x volume starting at row y0 - w_y lands in shared memory (rows outside
+// the image are zero-filled by the TMA unit: they never enter a window);
+// two stages, mbarrier-completed, refilled as soon as a stage is consumed.
+// Each warp scans SEG rows of the tile serially in registers (u64, exact),
+// segment offsets go through shared memory, the exact column prefix E lands in
+// shared memory, and every output pixel takes CA = E[y+N+1] - E[y-M] (O(1)
+// instead of O(W_y)) and keeps the running minimum with the paper's strict
+// "<": ties keep the smallest d.
 // ============================================================================
 struct YArgs {
-  const uint32_t* cax[2];
-  const uint32_t* arm[2];
-  uint8_t* Dmap[2];
-  uint64_t* ca[2];  // debug (may be null)
-  int Ws, Hs, Ds, Wp, w_y, B, T;
+  const uint32_t* arm0;
+  const uint32_t* arm1;
+  uint8_t* D0;
+  uint8_t* D1;
+  uint64_t* ca0;  // debug (may be null)
+  uint64_t* ca1;
+  int Ws, Hs, Ds, w_y, B;
 };
 
 constexpr int kYWarps = 8;
+constexpr int kYRPT = 12;  // output rows per thread (B <= 96)
+constexpr int kYStages = 2;
 
-template <int S, int RPT>
-__global__ void __launch_bounds__(kYWarps * 32) ypass_kernel(YArgs a) {
-  extern __shared__ uint64_t ysm[];
-  const int T = a.T;
-  uint64_t* sE = ysm;                        // [2][T+1][32]
-  uint64_t* sTot = ysm + 2 * (T + 1) * 32;   // [2][kYWarps][32]
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+template <int SEG>
+__global__ void __launch_bounds__(kYWarps * 32, 2)
+    ypass_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                 YArgs a) {
+  constexpr int TB = kYWarps * SEG;  // tile rows = TMA box height
+  constexpr uint32_t kTileBytes = TB * 32 * 4;
+  extern __shared__ uint8_t ysm_raw[];
+  uint8_t* ysm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ysm_raw) + 127) & ~uintptr_t(127));
+  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                      // [kYStages][TB][32]
+  uint64_t* E = reinterpret_cast<uint64_t*>(ysm + kYStages * kTileBytes);  // [TB+1][32]
+  uint64_t* tot = E + (TB + 1) * 32;                                       // [kYWarps][32]
+  uint64_t* bar = tot + kYWarps * 32;                                      // [kYStages]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int base = blockIdx.z;
-  const uint32_t* cax = base ? a.cax[1] : a.cax[0];
-  const uint32_t* armp = base ? a.arm[1] : a.arm[0];
-  uint64_t* cadbg = base ? a.ca[1] : a.ca[0];
-  uint8_t* dmap = base ? a.Dmap[1] : a.Dmap[0];
-  const int x = blockIdx.x * 32 + lane;
-  const int y0 = blockIdx.y * a.B;
-  const int yt0 = y0 - a.w_y;
-  const bool xin = x < a.Ws;
+  const CUtensorMap* tm = base ? &tm1 : &tm0;
+  const uint32_t* armp = base ? a.arm1 : a.arm0;
+  uint8_t* dmap = base ? a.D1 : a.D0;
+  uint64_t* cadbg = base ? a.ca1 : a.ca0;
+  const int x0 = blockIdx.x * 32, x = x0 + lane;
+  const int y0 = blockIdx.y * a.B, yt0 = y0 - a.w_y;
+  const int Ds = a.Ds;
 
-  // output rows of this thread and their window indices into E
-  int ia[RPT], ib[RPT];
-  uint64_t best[RPT];
-  int bd[RPT];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int y = y0 + w * RPT + r;
-    ia[r] = 0; ib[r] = 0; best[r] = ~0ull; bd[r] = 0;
-    if (xin && y < a.Hs && w * RPT + r < a.B) {
-      const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
-      const int M = (arm >> 16) & 255u, N = arm >> 24;
-      ia[r] = y - M - yt0;
-      ib[r] = y + N + 1 - yt0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kYStages && s < Ds; ++s) {
+      mbar_expect_tx(bar + s, kTileBytes);
+      tma_load_3d(tile + s * TB * 32, tm, bar + s, x0, yt0, s);
     }
   }
-  const int seg0 = w * S;
-  uint32_t v[S];
-  auto load = [&](int d) {
+  if (w == 0) E[lane] = 0;
+
+  // window byte offsets into E (d-invariant) and running minima
+  uint32_t oa[kYRPT], ob[kYRPT];
+  uint64_t best[kYRPT];
+  int bd[kYRPT];
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int yg = yt0 + seg0 + s;
-      v[s] = 0;
-      if (seg0 + s < T && yg >= 0 && yg < a.Hs)
-        v[s] = __ldg(cax + ((size_t)d * a.Hs + yg) * a.Wp + x);
+  for (int r = 0; r < kYRPT; ++r) {
+    const int yl = w * kYRPT + r, y = y0 + yl;
+    oa[r] = lane * 8u;
+    ob[r] = lane * 8u;
+    best[r] = ~0ull;
+    bd[r] = 0;
+    if (yl < a.B && y < a.Hs && x < a.Ws) {
+      const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
+      const int M = (arm >> 16) & 255u, N = arm >> 24;
+      oa[r] = ((uint32_t)(y - M - yt0) * 32u + lane) * 8u;
+      ob[r] = ((uint32_t)(y + N + 1 - yt0) * 32u + lane) * 8u;
     }
-  };
-  load(0);
-  for (int d = 0; d < a.Ds; ++d) {
-    const int buf = d & 1;
-    uint64_t loc[S];
+  }
+  const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
+  uint64_t* Ew = E + (w * SEG + 1) * 32 + lane;
+
+#pragma unroll 1
+  for (int d = 0; d < Ds; ++d) {
+    const int st = d & 1;
+    mbar_wait(bar + st, (d >> 1) & 1);
+    const uint32_t* tl = tile + st * TB * 32 + w * SEG * 32 + lane;
+    uint64_t loc[SEG];
     uint64_t acc = 0;
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      acc += v[s];
+    for (int s = 0; s < SEG; ++s) {
+      acc += tl[s * 32];
       loc[s] = acc;
     }
-    sTot[(buf * kYWarps + w) * 32 + lane] = acc;
-    __syncthreads();
+    tot[w * 32 + lane] = acc;
+    __syncthreads();  // (1) tile[st] consumed, segment totals visible
+    if (threadIdx.x == 0 && d + kYStages < Ds) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar + st, kTileBytes);
+      tma_load_3d(tile + st * TB * 32, tm, bar + st, x0, yt0, d + kYStages);
+    }
     uint64_t off = 0;
-    for (int q = 0; q < w; ++q) off += sTot[(buf * kYWarps + q) * 32 + lane];
-    uint64_t* E = sE + (size_t)buf * (T + 1) * 32;
-    if (w == 0) E[lane] = 0;
+    for (int q = 0; q < w; ++q) off += tot[q * 32 + lane];
 #pragma unroll
-    for (int s = 0; s < S; ++s)
-      if (seg0 + s < T) E[(seg0 + s + 1) * 32 + lane] = loc[s] + off;
-    if (d + 1 < a.Ds) load(d + 1);
-    __syncthreads();
+    for (int s = 0; s < SEG; ++s) Ew[s * 32] = loc[s] + off;
+    __syncthreads();  // (2) column prefix complete
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const uint64_t ca = E[ib[r] * 32 + lane] - E[ia[r] * 32 + lane];
+    for (int r = 0; r < kYRPT; ++r) {
+      const uint64_t ca = *reinterpret_cast<const uint64_t*>(Eb + ob[r]) -
+                          *reinterpret_cast<const uint64_t*>(Eb + oa[r]);
       if (ca < best[r]) { best[r] = ca; bd[r] = d; }
-      if (cadbg) {
-        const int y = y0 + w * RPT + r;
-        if (xin && y < a.Hs && w * RPT + r < a.B) cadbg[((size_t)d * a.Hs + y) * a.Ws + x] = ca;
+    }
+    if (cadbg) {
+#pragma unroll
+      for (int r = 0; r < kYRPT; ++r) {
+        const int yl = w * kYRPT + r, y = y0 + yl;
+        if (yl < a.B && y < a.Hs && x < a.Ws)
+          cadbg[((size_t)d * a.Hs + y) * a.Ws + x] =
+              *reinterpret_cast<const uint64_t*>(Eb + ob[r]) -
+              *reinterpret_cast<const uint64_t*>(Eb + oa[r]);
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int y = y0 + w * RPT + r;
-    if (xin && y < a.Hs && w * RPT + r < a.B) dmap[(size_t)y * a.Ws + x] = (uint8_t)bd[r];
+  for (int r = 0; r < kYRPT; ++r) {
+    const int yl = w * kYRPT + r, y = y0 + yl;
+    if (yl < a.B && y < a.Hs && x < a.Ws) dmap[(size_t)y * a.Ws + x] = (uint8_t)bd[r];
   }
 }
 
-constexpr int kYRPT = 8;
-constexpr int kYB = kYWarps * kYRPT;  // 64 output rows per tile
-
-static size_t ypass_smem_bytes(int T) {
-  return sizeof(uint64_t) * ((size_t)2 * (T + 1) * 32 + 2 * kYWarps * 32);
-}
-
-#define YPASS_DISPATCH(S_, EXPR)                             \
-  switch (S_) {                                              \
-    case 8: { constexpr int SS = 8; EXPR; } break;           \
-    case 16: { constexpr int SS = 16; EXPR; } break;         \
-    case 24: { constexpr int SS = 24; EXPR; } break;         \
-    case 32: { constexpr int SS = 32; EXPR; } break;         \
-    default: break;                                          \
+#define YPASS_DISPATCH(S_, EXPR)                       \
+  switch (S_) {                                        \
+    case 8: { constexpr int SS = 8; EXPR; } break;     \
+    case 12: { constexpr int SS = 12; EXPR; } break;   \
+    case 16: { constexpr int SS = 16; EXPR; } break;   \
+    case 20: { constexpr int SS = 20; EXPR; } break;   \
+    case 24: { constexpr int SS = 24; EXPR; } break;   \
+    case 28: { constexpr int SS = 28; EXPR; } break;   \
+    case 32: { constexpr int SS = 32; EXPR; } break;   \
+    default: break;                                    \
   }
 
-static int ypass_S_for(int T) {
+static int ypass_seg_for(int T) {
   const int need = (T + kYWarps - 1) / kYWarps;
-  for (int s : {8, 16, 24, 32})
+  for (int s : {8, 12, 16, 20, 24, 28, 32})
     if (s >= need) return s;
   return 0;
+}
+
+static int ypass_smem_bytes(int SEG) {
+  const int TB = kYWarps * SEG;
+  return kYStages * TB * 32 * 4 + (TB + 1) * 32 * 8 + kYWarps * 32 * 8 + kYStages * 8 + 128;
 }
 
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
                          cudaStream_t s) {
   YArgs a;
-  a.cax[0] = b.caxL; a.cax[1] = b.caxR;
-  a.arm[0] = b.armL; a.arm[1] = b.armR;
-  a.Dmap[0] = b.DL; a.Dmap[1] = b.DR;
-  a.ca[0] = store_ca ? b.caL : nullptr;
-  a.ca[1] = store_ca ? b.caR : nullptr;
-  a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.Wp = g.Wp; a.w_y = g.w_y;
-  a.B = p.ypass_B; a.T = p.ypass_T;
-  dim3 grid((g.Ws + 31) / 32, (g.Hs + p.ypass_B - 1) / p.ypass_B, 2);
+  a.arm0 = b.armL; a.arm1 = b.armR;
+  a.D0 = b.DL; a.D1 = b.DR;
+  a.ca0 = store_ca ? b.caL : nullptr;
+  a.ca1 = store_ca ? b.caR : nullptr;
+  a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
+  dim3 grid((g.Ws + 31) / 32, p.ypass_nb, 2);
   cudaError_t e = cudaErrorInvalidValue;
-  YPASS_DISPATCH(ypass_S_for(p.ypass_T),
-                 (ypass_kernel<SS, kYRPT><<<grid, kYWarps * 32, p.ypass_smem, s>>>(a),
+  YPASS_DISPATCH(p.ypass_SEG,
+                 (ypass_kernel<SS><<<grid, kYWarps * 32, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
                   e = cudaGetLastError()));
   return e;
 }
 
 // ============================================================================
-// CCMED — cross-check (Eq. 10; Step6 P:504-511; reading E5: the
-// partner is D^R[y][x-k]) fused with the 3x3 median on the masked left map
-// (Step7 first half; readings R21-R23).  A 34x10 masked tile (1-px
-// clamped halo) is built in shared memory; each pixel sorts its 9 clamped
-// neighbours with a 25-comparator network in registers (INVALID = 255 sorts
-// last) and takes sorted[(n_valid-1)/2].  Per-row first/last valid column are
-// recorded (warp ballot + one atomic per warp) for FILL rule (d).
+// POST — one CTA per scaled row y:
+//  * cross-check (Eq. 10; Step6 P:504-511; reading E5: the partner
+//    is D^R[y][x-k]) for the masked rows y-1 .. y+2 (clamped);
+//  * 3x3 median of the valid values (Step7 first half; R21-R23)
+//    for rows y and y+1, a 25-comparator sorting network in registers with
+//    INVALID = 255 sorting last, output sorted[(n_valid-1)/2];
+//  * bilateral fill (§III.E steps 1-3; Step7 P:516-525) of rows y
+//    and y+1: nearest valid neighbours from per-32-pixel ballot masks and a
+//    warp scan over the chunk summaries, then (a) (Dl*j + Dr*i)/(i+j) as one
+//    IEEE binary32 division (R26, sign reading E6), (b) brightness-closer
+//    side (tie -> left, R24), (c) one-sided copy;
+//  * scale-up (Step8; R27-R30) of output rows 2y, 2y+1 (K = 2), or
+//    the fill row itself as the output (K = 1).
+// Rows without any valid pixel (rule (d)) are patched by the last CTA to
+// finish (grid-wide counter), which sees every row's first/last valid column.
 // ============================================================================
+struct PostArgs {
+  const uint8_t* DL;
+  const uint8_t* DR;
+  const uint16_t* pixL;
+  const uint8_t* Lorg;
+  uint8_t* masked;
+  uint8_t* median;
+  float* fill;
+  float* out;
+  int32_t* rowFirst;
+  int32_t* rowLast;
+  unsigned* counter;
+  int W, H, Ws, Hs, K, T;
+  int Wsp;  // Ws rounded up to 32
+};
+
 __device__ __forceinline__ void cswap(int& a, int& b) {
   const int lo = min(a, b), hi = max(a, b);
-  a = lo; b = hi;
+  a = lo;
+  b = hi;
 }
 
-__global__ void __launch_bounds__(256) ccmed_kernel(const uint8_t* __restrict__ DL,
-                                                    const uint8_t* __restrict__ DR,
-                                                    uint8_t* __restrict__ masked,
-                                                    uint8_t* __restrict__ median,
-                                                    int32_t* rowFirst, int32_t* rowLast,
-                                                    int Ws, int Hs) {
-  __shared__ uint8_t t[10][34];
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int i = tid; i < 340; i += 256) {
-    const int r = i / 34, c = i % 34;
-    const int yy = clampi(y0 - 1 + r, 0, Hs - 1), xx = clampi(x0 - 1 + c, 0, Ws - 1);
-    const int k = __ldg(DL + (size_t)yy * Ws + xx);
-    const bool gcp = (xx - k >= 0) && (__ldg(DR + (size_t)yy * Ws + xx - k) == k);
-    t[r][c] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+// Step8 x rule on seeded row `f` (fill values) with original-resolution row `L`
+__device__ __forceinline__ float su_xval(const float* f, const uint8_t* __restrict__ L, int X,
+                                         int W, int Ws, float thr) {
+  if ((X & 1) == 0) {
+    if ((X >> 1) < Ws) return 2.0f * f[X >> 1];
+    X -= 1;  // extra last column of an odd width copies its predecessor
+  }
+  const float av = 2.0f * f[(X - 1) >> 1];
+  if (X + 1 < W && ((X + 1) >> 1) < Ws) {
+    const float bv = 2.0f * f[(X + 1) >> 1];
+    if (fabsf(__fsub_rn(av, bv)) <= thr) return __fmul_rn(__fadd_rn(av, bv), 0.5f);
+    const int c = __ldg(L + X);
+    return (abs((int)__ldg(L + X - 1) - c) <= abs((int)__ldg(L + X + 1) - c)) ? av : bv;
+  }
+  return av;
+}
+
+// bilateral fill value of pixel x given its nearest valid neighbours li / ri
+__device__ __forceinline__ float fill_value(const uint8_t* md, const uint16_t* __restrict__ pix,
+                                            int x, int li, int ri, int T) {
+  if (li >= 0 && ri >= 0) {
+    const int Dl = md[li], Dr = md[ri];
+    const int i = x - li, j = ri - x;
+    if (abs(Dl - Dr) <= T) return __fdiv_rn((float)(Dl * j + Dr * i), (float)(i + j));
+    const int cI = __ldg(pix + x) & 255, lI = __ldg(pix + li) & 255, rI = __ldg(pix + ri) & 255;
+    return (abs(lI - cI) <= abs(rI - cI)) ? (float)Dl : (float)Dr;
+  }
+  if (li >= 0) return (float)md[li];
+  if (ri >= 0) return (float)md[ri];
+  return 0.0f;  // no valid pixel in the row: patched by rule (d)
+}
+
+// rule (d) value for an all-invalid row r (reads other rows: global memory)
+__device__ float rule_d_value(const PostArgs& a, int r) {
+  for (int yy = r - 1; yy >= 0; --yy) {
+    const int l = __ldcg(a.rowLast + yy);
+    if (l >= 0) return (float)__ldcg(a.median + (size_t)yy * a.Ws + l);
+  }
+  for (int yy = r + 1; yy < a.Hs; ++yy) {
+    const int f = __ldcg(a.rowFirst + yy);
+    if (f >= 0) return (float)__ldcg(a.median + (size_t)yy * a.Ws + f);
+  }
+  return 0.0f;
+}
+
+// scale-up of output row Y from the (global) fill buffer — used by the rule-(d) patch
+__device__ void su_row_global(const PostArgs& a, int Y, float thr) {
+  const int Hs = a.Hs;
+  int ya, yb = -1;
+  if ((Y & 1) == 0 && (Y >> 1) < Hs) {
+    ya = Y >> 1;
+  } else if ((Y & 1) == 1 && Y + 1 < a.H && ((Y + 1) >> 1) < Hs) {
+    ya = (Y - 1) >> 1;
+    yb = (Y + 1) >> 1;
+  } else {
+    ya = min((Y - 1) >> 1, Hs - 1);
+  }
+  for (int X = threadIdx.x; X < a.W; X += blockDim.x) {
+    float v = su_xval(a.fill + (size_t)ya * a.Ws, a.Lorg + (size_t)(2 * ya) * a.W, X, a.W, a.Ws, thr);
+    if (yb >= 0)
+      v = __fmul_rn(__fadd_rn(v, su_xval(a.fill + (size_t)yb * a.Ws,
+                                         a.Lorg + (size_t)(2 * yb) * a.W, X, a.W, a.Ws, thr)),
+                    0.5f);
+    a.out[(size_t)Y * a.W + X] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
+  extern __shared__ uint32_t psm_[];
+  const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5;
+  uint8_t* mk = reinterpret_cast<uint8_t*>(psm_);                // [4][Wsp] masked rows y-1..y+2
+  uint8_t* md = mk + 4 * Wsp;                                    // [2][Wsp] median rows y, y+1
+  float* fv = reinterpret_cast<float*>(md + 2 * Wsp);            // [2][Wsp] fill rows y, y+1
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(fv + 2 * Wsp);   // [2][64]
+  int* prevLast = reinterpret_cast<int*>(cmask + 128);           // [2][64]
+  int* nextFirst = prevLast + 128;                               // [2][64]
+  __shared__ int s_last;
+  const int y = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrows = (a.K == 2 && y + 1 < a.Hs) ? 2 : 1;
+  const float thr = (float)(a.K * a.T);
+
+  // 1. masked rows y-1 .. y+nrows (clamped rows, Eq. 10)
+  for (int i = tid; i < (nrows + 2) * Ws; i += blockDim.x) {
+    const int r = i / Ws, x = i - r * Ws;
+    const int yy = clampi(y - 1 + r, 0, a.Hs - 1);
+    const int k = __ldg(a.DL + (size_t)yy * Ws + x);
+    const bool gcp = (x - k >= 0) && (__ldg(a.DR + (size_t)yy * Ws + x - k) == k);
+    mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
   }
   __syncthreads();
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int x = x0 + tx, y = y0 + ty;
-  const bool in = x < Ws && y < Hs;
-  int out = kInvalid;
-  if (in) {
-    const int c = t[ty + 1][tx + 1];
+  // 2. median rows y, y+1
+  for (int i = tid; i < nrows * Ws; i += blockDim.x) {
+    const int j = i / Ws, x = i - j * Ws;
+    const int c = mk[(j + 1) * Wsp + x];
+    int out = kInvalid;
     if (c != kInvalid) {
-      int v0 = t[ty][tx], v1 = t[ty][tx + 1], v2 = t[ty][tx + 2];
-      int v3 = t[ty + 1][tx], v4 = c, v5 = t[ty + 1][tx + 2];
-      int v6 = t[ty + 2][tx], v7 = t[ty + 2][tx + 1], v8 = t[ty + 2][tx + 2];
-      const int n = (v0 != kInvalid) + (v1 != kInvalid) + (v2 != kInvalid) + (v3 != kInvalid) +
-                    1 + (v5 != kInvalid) + (v6 != kInvalid) + (v7 != kInvalid) + (v8 != kInvalid);
-      // 9-input sorting network (25 compare-exchanges)
+      const int xl = max(x - 1, 0), xr = min(x + 1, Ws - 1);
+      const uint8_t* r0 = mk + j * Wsp;
+      const uint8_t* r1 = r0 + Wsp;
+      const uint8_t* r2 = r1 + Wsp;
+      int v0 = r0[xl], v1 = r0[x], v2 = r0[xr];
+      int v3 = r1[xl], v4 = c, v5 = r1[xr];
+      int v6 = r2[xl], v7 = r2[x], v8 = r2[xr];
+      const int n = (v0 != kInvalid) + (v1 != kInvalid) + (v2 != kInvalid) + (v3 != kInvalid) + 1 +
+                    (v5 != kInvalid) + (v6 != kInvalid) + (v7 != kInvalid) + (v8 != kInvalid);
       cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
       cswap(v1, v2); cswap(v4, v5); cswap(v7, v8);
       cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
@@ -501,196 +709,226 @@ __global__ void __launch_bounds__(256) ccmed_kernel(const uint8_t* __restrict__ 
       cswap(v1, v3); cswap(v5, v7); cswap(v2, v6);
       cswap(v4, v6); cswap(v2, v4); cswap(v2, v3);
       cswap(v5, v6);
-      const int k = (n - 1) >> 1;  // 0..4
-      out = k == 0 ? v0 : k == 1 ? v1 : k == 2 ? v2 : k == 3 ? v3 : v4;
+      const int kk = (n - 1) >> 1;  // 0..4
+      out = kk == 0 ? v0 : kk == 1 ? v1 : kk == 2 ? v2 : kk == 3 ? v3 : v4;
     }
-    const size_t o = (size_t)y * Ws + x;
-    masked[o] = (uint8_t)c;
-    median[o] = (uint8_t)out;
-  }
-  const unsigned bal = __ballot_sync(kFull, in && out != kInvalid);
-  if (tx == 0 && bal && y < Hs) {
-    atomicMin(rowFirst + y, x0 + __ffs(bal) - 1);
-    atomicMax(rowLast + y, x0 + 31 - __clz(bal));
-  }
-}
-
-cudaError_t launch_ccmed(const Geom& g, Buffers& b, cudaStream_t s) {
-  dim3 grid((g.Ws + 31) / 32, (g.Hs + 7) / 8);
-  ccmed_kernel<<<grid, dim3(32, 8), 0, s>>>(b.DL, b.DR, b.masked, b.median, b.rowFirst,
-                                             b.rowLast, g.Ws, g.Hs);
-  return cudaGetLastError();
-}
-
-// ============================================================================
-// FILL — bilateral estimation of non-GCPs (§III.E steps 1-3; Step7
-// P:516-525), one warp per row.  Nearest valid neighbours by ballot scans
-// (left: forward pass with carry; right: backward pass), then
-//  (a) |Dl-Dr| <= T: (Dl*j + Dr*i)/(i+j), one IEEE binary32 division (R26; the
-//      sign of Eq. 11 as printed is reading E6);
-//  (b) else the side whose scaled-L brightness is closer (tie -> left, R24);
-//  (c) one-sided -> that side;  (d) all-invalid row -> last valid value of the
-//      nearest row above, else first valid of the nearest row below, else 0.
-// ============================================================================
-__global__ void __launch_bounds__(256) fill_kernel(const uint8_t* __restrict__ median,
-                                                   const uint16_t* __restrict__ pixL,
-                                                   const int32_t* __restrict__ rowFirst,
-                                                   const int32_t* __restrict__ rowLast,
-                                                   float* __restrict__ out, int Ws, int Hs,
-                                                   int T) {
-  extern __shared__ int16_t fsm[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int y = blockIdx.x * 8 + w;
-  if (y >= Hs) return;
-  int16_t* sLeft = fsm + w * Ws;
-  const uint8_t* med = median + (size_t)y * Ws;
-  const uint16_t* pix = pixL + (size_t)y * Ws;
-  float* o = out + (size_t)y * Ws;
-  const int nch = (Ws + 31) / 32;
-  int carry = -1;
-  for (int c = 0; c < nch; ++c) {
-    const int x = c * 32 + lane;
-    const bool valid = x < Ws && med[x] != kInvalid;
-    const unsigned mask = __ballot_sync(kFull, valid);
-    const unsigned below = mask & ((1u << lane) - 1u);
-    if (x < Ws) sLeft[x] = (int16_t)(below ? c * 32 + 31 - __clz(below) : carry);
-    if (mask) carry = c * 32 + 31 - __clz(mask);
-  }
-  if (carry < 0) {  // rule (d): no valid pixel in this row
-    int v = 0;
-    if (lane == 0) {
-      bool found = false;
-      for (int yy = y - 1; yy >= 0 && !found; --yy)
-        if (rowLast[yy] >= 0 && rowLast[yy] < Ws) { v = median[(size_t)yy * Ws + rowLast[yy]]; found = true; }
-      for (int yy = y + 1; yy < Hs && !found; ++yy)
-        if (rowFirst[yy] >= 0 && rowFirst[yy] < Ws) { v = median[(size_t)yy * Ws + rowFirst[yy]]; found = true; }
+    md[j * Wsp + x] = (uint8_t)out;
+    if (j == 0) {
+      a.masked[(size_t)y * Ws + x] = (uint8_t)c;
+      a.median[(size_t)y * Ws + x] = (uint8_t)out;
     }
-    v = __shfl_sync(kFull, v, 0);
-    for (int x = lane; x < Ws; x += 32) o[x] = (float)v;
-    return;
   }
-  __syncwarp();
-  int rcarry = -1;
-  for (int c = nch - 1; c >= 0; --c) {
-    const int x = c * 32 + lane;
-    const bool valid = x < Ws && med[x] != kInvalid;
-    const unsigned mask = __ballot_sync(kFull, valid);
-    const unsigned above = lane == 31 ? 0u : (mask & ~((2u << lane) - 1u));
-    const int ri = above ? c * 32 + __ffs(above) - 1 : rcarry;
-    if (x < Ws) {
-      float val;
-      if (valid) {
-        val = (float)med[x];
-      } else {
-        const int li = sLeft[x];
-        if (li >= 0 && ri >= 0) {
-          const int Dl = med[li], Dr = med[ri];
-          const int i = x - li, j = ri - x;
-          if (abs(Dl - Dr) <= T) {
-            val = __fdiv_rn((float)(Dl * j + Dr * i), (float)(i + j));
-          } else {
-            const int cI = pix[x] & 255, lI = pix[li] & 255, rI = pix[ri] & 255;
-            val = (abs(lI - cI) <= abs(rI - cI)) ? (float)Dl : (float)Dr;
-          }
-        } else if (li >= 0) {
-          val = (float)med[li];
-        } else {
-          val = (float)med[ri];
-        }
+  __syncthreads();
+  // 3. per-32-pixel validity masks
+  for (int c = warp; c < nrows * nch; c += blockDim.x >> 5) {
+    const int j = c / nch, cc = c - j * nch;
+    const int x = cc * 32 + lane;
+    const unsigned m = __ballot_sync(kFull, x < Ws && md[j * Wsp + x] != kInvalid);
+    if (lane == 0) cmask[j * 64 + cc] = m;
+  }
+  __syncthreads();
+  // 4. warp j: exclusive max-scan of chunk last-valid, reverse min-scan of first-valid
+  if (warp < nrows) {
+    const int j = warp;
+    int carry = -1;
+    for (int base = 0; base < nch; base += 32) {
+      const int cc = base + lane;
+      const unsigned m = cc < nch ? cmask[j * 64 + cc] : 0u;
+      int v = m ? cc * 32 + 31 - __clz(m) : -1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v = max(v, t);
       }
-      o[x] = val;
+      const int prev = __shfl_up_sync(kFull, v, 1);
+      if (cc < nch) prevLast[j * 64 + cc] = lane == 0 ? carry : max(carry, prev);
+      carry = max(carry, __shfl_sync(kFull, v, 31));
     }
-    if (mask) rcarry = c * 32 + __ffs(mask) - 1;
+    if (j == 0 && lane == 0) a.rowLast[y] = carry;
+    int rc = INT_MAX;  // INT_MAX = none
+    for (int base = ((nch - 1) >> 5) << 5; base >= 0; base -= 32) {
+      const int cc = base + lane;
+      const unsigned m = cc < nch ? cmask[j * 64 + cc] : 0u;
+      int v = m ? cc * 32 + __ffs(m) - 1 : INT_MAX;
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive min-scan toward lower lanes
+        const int t = __shfl_down_sync(kFull, v, o);
+        if (lane + o < 32) v = min(v, t);
+      }
+      const int nxt = __shfl_down_sync(kFull, v, 1);
+      const int excl = lane == 31 ? rc : min(nxt, rc);
+      if (cc < nch) nextFirst[j * 64 + cc] = excl == INT_MAX ? -1 : excl;
+      rc = min(rc, __shfl_sync(kFull, v, 0));
+    }
+    if (j == 0 && lane == 0) a.rowFirst[y] = rc == INT_MAX ? -1 : rc;
   }
+  __syncthreads();
+  // 5. fill values of rows y, y+1
+  for (int i = tid; i < nrows * Wsp; i += blockDim.x) {
+    const int j = i / Wsp, x = i - j * Wsp;
+    if (x >= Ws) continue;
+    const uint8_t* mdr = md + j * Wsp;
+    float v;
+    if (mdr[x] != kInvalid) {
+      v = (float)mdr[x];
+    } else {
+      const int cc = x >> 5, ln = x & 31;
+      const unsigned m = cmask[j * 64 + cc];
+      const unsigned below = m & ((1u << ln) - 1u);
+      const unsigned above = ln == 31 ? 0u : (m & ~((2u << ln) - 1u));
+      const int li = below ? cc * 32 + 31 - __clz(below) : prevLast[j * 64 + cc];
+      const int ri = above ? cc * 32 + __ffs(above) - 1 : nextFirst[j * 64 + cc];
+      v = fill_value(mdr, a.pixL + (size_t)(y + j) * Ws, x, li, ri, a.T);
+    }
+    fv[j * Wsp + x] = v;
+    if (j == 0) {
+      if (a.K == 2) a.fill[(size_t)y * Ws + x] = v;
+      else a.out[(size_t)y * Ws + x] = v;
+    }
+  }
+  if (a.K == 2) {
+    __syncthreads();
+    // 6. scale-up: output rows 2y, 2y+1 (+ the extra last row of an odd H)
+    const uint8_t* L0 = a.Lorg + (size_t)(2 * y) * a.W;
+    const uint8_t* L1 = a.Lorg + (size_t)(2 * min(y + 1, a.Hs - 1)) * a.W;
+    for (int X = tid; X < a.W; X += blockDim.x) {
+      const float v0 = su_xval(fv, L0, X, a.W, Ws, thr);
+      a.out[(size_t)(2 * y) * a.W + X] = v0;
+      if (2 * y + 1 < a.H) {
+        float v1 = v0;
+        if (nrows == 2) v1 = __fmul_rn(__fadd_rn(v0, su_xval(fv + Wsp, L1, X, a.W, Ws, thr)), 0.5f);
+        a.out[(size_t)(2 * y + 1) * a.W + X] = v1;
+        if (y == a.Hs - 1 && 2 * y + 2 < a.H) a.out[(size_t)(2 * y + 2) * a.W + X] = v1;
+      }
+    }
+  }
+  // 7. rule (d): the last CTA patches rows with no valid pixel
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  bool any = false;
+  for (int r = 0; r < a.Hs; ++r) {
+    if (__ldcg(a.rowLast + r) >= 0) continue;
+    any = true;
+    const float v = rule_d_value(a, r);
+    float* dst = (a.K == 2 ? a.fill : a.out) + (size_t)r * Ws;
+    for (int x = tid; x < Ws; x += blockDim.x) dst[x] = v;
+  }
+  if (any && a.K == 2) {
+    __threadfence();
+    __syncthreads();
+    for (int r = 0; r < a.Hs; ++r) {
+      if (__ldcg(a.rowLast + r) >= 0) continue;
+      for (int Y = max(2 * r - 1, 0); Y <= min(2 * r + 2, a.H - 1); ++Y) su_row_global(a, Y, thr);
+    }
+  }
+  if (tid == 0) *a.counter = 0u;
 }
 
-cudaError_t launch_fill(const Geom& g, Buffers& b, float* out, cudaStream_t s) {
-  const size_t smem = sizeof(int16_t) * 8 * g.Ws;
-  fill_kernel<<<(g.Hs + 7) / 8, 256, smem, s>>>(b.median, b.pixL, b.rowFirst, b.rowLast, out,
-                                                g.Ws, g.Hs, g.t_fill);
-  return cudaGetLastError();
-}
-
-// ============================================================================
-// SU — Step8: values x K on the even grid (R27); odd columns of
-// seeded rows by the bilateral rule with i = j = 1 and threshold K*T (R28),
-// brightness from L_org; odd rows linear (mean of the neighbouring seeded
-// rows, R30); a missing successor copies its predecessor.  One thread per
-// output pixel, each recomputing the seeded-row values it needs (idempotent,
-// binary32 round-to-nearest intrinsics: bit-identical to the oracle).
-// ============================================================================
-__device__ __forceinline__ float su_xval(const float* __restrict__ v,
-                                         const uint8_t* __restrict__ Lorg, int X, int y, int W,
-                                         int Ws, float thr) {
-  const float* row = v + (size_t)y * Ws;
-  if ((X & 1) == 0) {
-    if ((X >> 1) < Ws) return 2.0f * __ldg(row + (X >> 1));
-    X -= 1;  // extra last column of an odd width: copy the predecessor
-  }
-  const float a = 2.0f * __ldg(row + ((X - 1) >> 1));
-  if (X + 1 < W && ((X + 1) >> 1) < Ws) {
-    const float b = 2.0f * __ldg(row + ((X + 1) >> 1));
-    if (fabsf(__fsub_rn(a, b)) <= thr) return __fmul_rn(__fadd_rn(a, b), 0.5f);
-    const uint8_t* lr = Lorg + (size_t)(2 * y) * W;
-    const int c = __ldg(lr + X);
-    return (abs((int)__ldg(lr + X - 1) - c) <= abs((int)__ldg(lr + X + 1) - c)) ? a : b;
-  }
-  return a;
-}
-
-__global__ void __launch_bounds__(256) su_kernel(const float* __restrict__ v,
-                                                 const uint8_t* __restrict__ Lorg,
-                                                 float* __restrict__ out, int W, int H, int Ws,
-                                                 int Hs, float thr) {
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  const int Y = blockIdx.y;
-  if (X >= W) return;
-  float r;
-  if ((Y & 1) == 0 && (Y >> 1) < Hs) {
-    r = su_xval(v, Lorg, X, Y >> 1, W, Ws, thr);
-  } else if ((Y & 1) == 1 && Y + 1 < H && ((Y + 1) >> 1) < Hs) {
-    r = __fmul_rn(__fadd_rn(su_xval(v, Lorg, X, (Y - 1) >> 1, W, Ws, thr),
-                            su_xval(v, Lorg, X, (Y + 1) >> 1, W, Ws, thr)), 0.5f);
-  } else {
-    r = su_xval(v, Lorg, X, Hs - 1 < ((Y - 1) >> 1) ? Hs - 1 : ((Y - 1) >> 1), W, Ws, thr);
-  }
-  out[(size_t)Y * W + X] = r;
-}
-
-cudaError_t launch_su(const Geom& g, const float* fill, const uint8_t* Lorg, float* out,
-                      cudaStream_t s) {
-  dim3 grid((g.W + 255) / 256, g.H);
-  su_kernel<<<grid, 256, 0, s>>>(fill, Lorg, out, g.W, g.H, g.Ws, g.Hs,
-                                 (float)(g.K * g.t_fill));
+cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
+                        float* out, cudaStream_t s) {
+  PostArgs a;
+  a.DL = b.DL; a.DR = b.DR; a.pixL = b.pixL; a.Lorg = Lorg;
+  a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
+  a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
+  a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
+  a.Wsp = (g.Ws + 31) & ~31;
+  post_kernel<<<g.Hs, 256, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
 // ============================================================================
 // Launch planning (create time)
 // ============================================================================
-cudaError_t plan_kernels(const Geom& g, Plan& p, int device) {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess) return e;
+    if (q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
+    fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)g.Ds};
+  cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 4, (cuuint64_t)g.Wp * g.Hs * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) return e;
+  const int nsm = prop.multiProcessorCount;
+  // SD / PREP / POST dynamic shared memory
+  p.sd_smem = (2 * g.m_pool + 1) * ((g.W + 3) & ~3) + 16;
+  {
+    int HX, HY, BWp, AHp;
+    prep_geometry(g, HX, HY, BWp, AHp);
+    p.prep_smem = 12 * BWp + 36 * AHp + 16;
+  }
+  const int Wsp = (g.Ws + 31) & ~31;
+  p.post_smem = 4 * Wsp + 2 * Wsp + 2 * Wsp * 4 + 3 * 128 * 4 + 64;
+  if (p.sd_smem > 48 * 1024) {
+    switch (g.m_pool) {
+      case 0: e = cudaFuncSetAttribute(sd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
+      case 1: e = cudaFuncSetAttribute(sd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
+      case 2: e = cudaFuncSetAttribute(sd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
+      default: e = cudaFuncSetAttribute(sd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  // XPASS
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
-  p.xpass_smem = (int)xpass_smem_bytes(p.xpass_C);
+  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x + 3;
+  p.xpass_smem = (int)(sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + 3 * 32 * p.xpass_C +
+                                           (size_t)kXWarps * p.xpass_PL));
   int occ = 0;
   XPASS_DISPATCH(p.xpass_C, (e = setup_xpass_c<CC>(p.xpass_smem), occ = occ_xpass_c<CC>(p.xpass_smem)));
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int units = g.Hs * ((g.Ds + kXDPerUnit - 1) / kXDPerUnit);
-  p.xpass_grid = units < occ * prop.multiProcessorCount ? units : occ * prop.multiProcessorCount;
-
-  p.ypass_B = kYB;
-  p.ypass_T = kYB + 2 * g.w_y;
-  if (!ypass_S_for(p.ypass_T)) return cudaErrorInvalidValue;
-  p.ypass_smem = (int)ypass_smem_bytes(p.ypass_T);
-  YPASS_DISPATCH(ypass_S_for(p.ypass_T),
-                 e = cudaFuncSetAttribute(ypass_kernel<SS, kYRPT>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          p.ypass_smem));
-  return e;
+  p.xpass_grid = units < occ * nsm ? units : occ * nsm;
+  // YPASS: choose the number of tiles per strip balancing halo cost and waves
+  const int strips = (g.Ws + 31) / 32;
+  const int nb0 = (g.Hs + kYWarps * kYRPT - 1) / (kYWarps * kYRPT);
+  double best = 1e30;
+  p.ypass_nb = 0;
+  for (int nb = nb0; nb <= g.Hs && nb <= 4 * nb0 + 8; ++nb) {
+    const int B = (g.Hs + nb - 1) / nb;
+    const int SEG = ypass_seg_for(B + 2 * g.w_y);
+    if (!SEG) continue;
+    const int smem = ypass_smem_bytes(SEG);
+    if (smem > 227 * 1024) continue;
+    const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
+    const int ctas = strips * nb * 2;
+    const double waves = (double)((ctas + nsm * per_sm - 1) / (nsm * per_sm));
+    const double cost = waves * per_sm * (6.0 * kYWarps * SEG + 10.0 * B);
+    if (cost < best - 1e-9) {
+      best = cost;
+      p.ypass_nb = nb; p.ypass_B = B; p.ypass_SEG = SEG; p.ypass_smem = smem;
+    }
+  }
+  if (!p.ypass_nb) return cudaErrorInvalidValue;
+  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       p.ypass_smem));
+  if (e != cudaSuccess) return e;
+  if ((e = make_tmap(&p.tmL, b.caxL, g, kYWarps * p.ypass_SEG))) return e;
+  if ((e = make_tmap(&p.tmR, b.caxR, g, kYWarps * p.ypass_SEG))) return e;
+  return cudaSuccess;
 }
 
 }  // namespace stereo

@@ -219,18 +219,18 @@ def test_stage_isolation_ypass_from_oracle_cax():
 
 
 def test_stage_isolation_post_from_oracle_maps():
+    """Feed the oracle's D^L / D^R into the fused post stage alone."""
     L, R, _ = synth.scene(160, 100, 32, seed=8)
     p = oracle.params()
-    ref = oracle.pipeline(L, R, 32, p, "fixed", stages=("DL", "DR", "masked", "median", "fill", "out", "Ls", "cenL"))
+    ref = oracle.pipeline(L, R, 32, p, "fixed",
+                          stages=("DL", "DR", "masked", "median", "fill", "out", "Ls", "cenL"))
     st = abi.Stereo(160, 100, 32)
     st.upload(abi.BUF_DL, ref["DL"])
     st.upload(abi.BUF_DR, ref["DR"])
     st.upload(abi.BUF_PIX_L, ref["Ls"].astype(np.uint16) | (ref["cenL"].astype(np.uint16) << 8))
     Lt = torch.from_numpy(L).to(DEV)
     out = torch.zeros((100, 160), dtype=torch.float32, device=DEV)
-    st.run_stage(abi.STAGE_CCMED)
-    st.run_stage(abi.STAGE_FILL)
-    st.run_stage(abi.STAGE_SU, L=Lt, out=out)
+    st.run_stage(abi.STAGE_POST, L=Lt, out=out)
     torch.cuda.synchronize()
     assert np.array_equal(st.download(abi.BUF_MASKED), ref["masked"])
     assert np.array_equal(st.download(abi.BUF_MEDIAN), ref["median"])
@@ -239,27 +239,33 @@ def test_stage_isolation_post_from_oracle_maps():
     st.close()
 
 
-def test_all_invalid_rows_rule_d():
-    """Rule (d): rows without any valid pixel (constructed via uploaded maps)."""
+@pytest.mark.parametrize("K", [1, 2])
+def test_all_invalid_rows_rule_d(K):
+    """Rule (d): rows without any valid pixel (constructed via uploaded maps),
+    including the first rows and an odd output height."""
     Ws, Hs = 40, 12
-    st = abi.Stereo(Ws, Hs, 8, k_scale=1)
+    W, H = Ws * K + (K - 1), Hs * K + (K - 1)
+    st = abi.Stereo(W, H, 8, k_scale=K)
     rng = np.random.default_rng(3)
     DL = rng.integers(0, 8, (Hs, Ws)).astype(np.uint8)
     DR = np.full((Hs, Ws), 200, np.uint8)  # nothing cross-checks ...
     for y in (4, 5, 9):                    # ... except rows 4, 5 and 9
-        DR[y] = 0
-        DL[y] = 0
-    L = rng.integers(0, 256, (Hs, Ws)).astype(np.uint8)
+        DR[y] = DL[y] = rng.integers(0, 3)
+        DL[y, :3] = 0
+        DR[y, :3] = 0
+    Ls = rng.integers(0, 256, (Hs, Ws)).astype(np.uint8)
+    Lorg = rng.integers(0, 256, (H, W)).astype(np.uint8)
     st.upload(abi.BUF_DL, DL)
     st.upload(abi.BUF_DR, DR)
-    st.upload(abi.BUF_PIX_L, L.astype(np.uint16))
-    out = torch.zeros((Hs, Ws), dtype=torch.float32, device=DEV)
-    st.run_stage(abi.STAGE_CCMED)
-    st.run_stage(abi.STAGE_FILL, out=out)
+    st.upload(abi.BUF_PIX_L, Ls.astype(np.uint16))
+    out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    Lt = torch.from_numpy(Lorg).to(DEV)
+    for _ in range(2):  # twice: the grid-wide counter must reset itself
+        st.run_stage(abi.STAGE_POST, L=Lt, out=out)
     torch.cuda.synchronize()
-    masked = oracle.cross_check(DL, DR)
-    med = oracle.median3x3(masked)
-    ref = oracle.fill_bilateral(med, L, 3)
+    med = oracle.median3x3(oracle.cross_check(DL, DR))
+    fill = oracle.fill_bilateral(med, Ls, 3)
+    ref = fill if K == 1 else oracle.scale_up(fill, Lorg, 2, 3)
     assert np.array_equal(out.cpu().numpy(), ref)
     st.close()
 
