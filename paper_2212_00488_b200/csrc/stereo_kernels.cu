@@ -103,23 +103,25 @@ struct PrepArgs {
   int8_t cdx[6], cdy[6];
 };
 
-__device__ __forceinline__ uint32_t ld4u(const uint8_t* p) {  // 4 bytes at any alignment
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-  return __funnelshift_r(q[0], q[1], (uint32_t)(a & 3) * 8u);
+// 4 bytes of a shared-memory byte array starting at byte offset `o` (any
+// alignment): two aligned word loads + funnel shift, staying in the shared
+// address space (no generic 64-bit addressing).
+__device__ __forceinline__ uint32_t ld4u(const uint32_t* s32, int o) {
+  const int w = o >> 2;
+  return __funnelshift_r(s32[w], s32[w + 1], (uint32_t)(o & 3) * 8u);
 }
-// similar run going forward: p[0] is the first neighbour
-__device__ __forceinline__ int run_fwd(const uint8_t* p, int lim, uint32_t c4, uint32_t d4) {
+// similar run going forward: byte o is the first neighbour
+__device__ __forceinline__ int run_fwd(const uint32_t* s32, int o, int lim, uint32_t c4, uint32_t d4) {
   for (int n = 0; n < lim; n += 4) {
-    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(p + n), c4), d4);
+    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(s32, o + n), c4), d4);
     if (ge) return min(n + ((__ffs(ge) - 1) >> 3), lim);
   }
   return lim;
 }
-// similar run going backward: p[-1] is the first neighbour
-__device__ __forceinline__ int run_bwd(const uint8_t* p, int lim, uint32_t c4, uint32_t d4) {
+// similar run going backward: byte o - 1 is the first neighbour
+__device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint32_t c4, uint32_t d4) {
   for (int n = 0; n < lim; n += 4) {
-    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(p - n - 4), c4), d4);
+    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(s32, o - n - 4), c4), d4);
     if (ge) return min(n + (__clz(ge) >> 3), lim);
   }
   return lim;
@@ -131,20 +133,20 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   uint8_t* sV = sB + 12 * a.BWp;                      // [36][AHp]  vertical strip, transposed
   const uint8_t* img = blockIdx.z ? a.img1 : a.img0;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
   const int HX = a.HX, HY = a.HY, BWp = a.BWp, AHp = a.AHp;
-  for (int i = tid; i < 12 * BWp; i += 256) {
-    const int r = i / BWp, c = i - r * BWp;
-    sB[i] = __ldg(img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws +
-                  clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 12; r += 8) {
+    const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws;
+    for (int c = tx; c < BWp; c += 32) sB[r * BWp + c] = __ldg(row + clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
   }
-  for (int i = tid; i < 36 * AHp; i += 256) {
-    const int r = i / 36, c = i - r * 36;  // consecutive threads: consecutive columns
-    sV[c * AHp + r] = __ldg(img + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws +
-                            clampi(x0 - 2 + c, 0, a.Ws - 1));
+  // transposed vertical strip: lane = image row (coalescing is irrelevant here,
+  // the rows are L1/L2 resident) so the shared stores are bank-conflict free
+  for (int c = ty; c < 36; c += 8) {
+    const uint8_t* col = img + clampi(x0 - 2 + c, 0, a.Ws - 1);
+    for (int r = tx; r < AHp; r += 32)
+      sV[c * AHp + r] = __ldg(col + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws);
   }
   __syncthreads();
-  const int tx = threadIdx.x, ty = threadIdx.y;
   const int x = x0 + tx, y = y0 + ty;
   if (x >= a.Ws || y >= a.Hs) return;
   const uint8_t* ctr = sB + (ty + 2) * BWp + tx + HX + 8;
@@ -158,11 +160,12 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
   } else {
     const uint32_t c4 = (uint32_t)c * 0x01010101u, d4 = (uint32_t)a.delta * 0x01010101u;
-    n = run_fwd(ctr + 1, min(a.w_x, a.Ws - 1 - x), c4, d4);
-    m = run_bwd(ctr, min(a.w_x, x), c4, d4);
-    const uint8_t* col = sV + (tx + 2) * AHp + ty + HY + 8;
-    N = run_fwd(col + 1, min(a.w_y, a.Hs - 1 - y), c4, d4);
-    M = run_bwd(col, min(a.w_y, y), c4, d4);
+    const int oB = (ty + 2) * BWp + tx + HX + 8;                 // centre in sB
+    const int oV = 12 * BWp + (tx + 2) * AHp + ty + HY + 8;      // centre in sV
+    n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, d4);
+    m = run_bwd(psm32, oB, min(a.w_x, x), c4, d4);
+    N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, d4);
+    M = run_bwd(psm32, oV, min(a.w_y, y), c4, d4);
   }
   const size_t o = (size_t)y * a.Ws + x;
   (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
@@ -418,8 +421,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 2)
                  YArgs a) {
   constexpr int TB = kYWarps * SEG;  // tile rows = TMA box height
   constexpr uint32_t kTileBytes = TB * 32 * 4;
-  extern __shared__ uint8_t ysm_raw[];
-  uint8_t* ysm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ysm_raw) + 127) & ~uintptr_t(127));
+  extern __shared__ __align__(128) uint8_t ysm[];  // TMA destinations need 128-B alignment
   uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                      // [kYStages][TB][32]
   uint64_t* E = reinterpret_cast<uint64_t*>(ysm + kYStages * kTileBytes);  // [TB+1][32]
   uint64_t* tot = E + (TB + 1) * 32;                                       // [kYWarps][32]
@@ -537,7 +539,7 @@ static int ypass_seg_for(int T) {
 
 static int ypass_smem_bytes(int SEG) {
   const int TB = kYWarps * SEG;
-  return kYStages * TB * 32 * 4 + (TB + 1) * 32 * 8 + kYWarps * 32 * 8 + kYStages * 8 + 128;
+  return kYStages * TB * 32 * 4 + (TB + 1) * 32 * 8 + kYWarps * 32 * 8 + kYStages * 8;
 }
 
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
@@ -807,6 +809,12 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  int mine = 0;  // parallel check first: almost always no row needs patching
+  for (int r = tid; r < a.Hs; r += blockDim.x) mine |= __ldcg(a.rowLast + r) < 0;
+  if (!__syncthreads_or(mine)) {
+    if (tid == 0) *a.counter = 0u;
+    return;
+  }
   bool any = false;
   for (int r = 0; r < a.Hs; ++r) {
     if (__ldcg(a.rowLast + r) >= 0) continue;
