@@ -257,7 +257,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   Geom& g = h->g;
   g.W = W; g.H = H; g.D = D; g.K = p->k_scale; g.m_pool = p->m_pool;
   g.Ws = W / g.K; g.Hs = H / g.K; g.Ds = (D + g.K - 1) / g.K;
-  g.Wp = (g.Ws + 31) / 32 * 32;
+  g.Wp = 32 * xpass_chunk_for(g.Ws);  // CA_x pitch = the x pass's lane-chunk span
   g.w_x = p->w_x; g.w_y = p->w_y; g.delta = p->delta; g.t_fill = p->t_fill;
   g.f = frac_bits(p->w_x);
   g.border = 1u << (g.f + 1);

@@ -103,28 +103,38 @@ struct PrepArgs {
   int8_t cdx[6], cdy[6];
 };
 
-// 4 bytes of a shared-memory byte array starting at byte offset `o` (any
-// alignment): two aligned word loads + funnel shift, staying in the shared
-// address space (no generic 64-bit addressing).
-__device__ __forceinline__ uint32_t ld4u(const uint32_t* s32, int o) {
-  const int w = o >> 2;
-  return __funnelshift_r(s32[w], s32[w + 1], (uint32_t)(o & 3) * 8u);
+// Byte-SIMD "dissimilar" test: bit 7 of byte i of the result is set iff byte
+// i of `diff` (an |dI|) is >= delta, for 1 <= delta <= 255.  dl4 replicates
+// delta (delta < 128) or delta - 128 (delta >= 128, `big`).  Three ALU ops:
+// ((diff & 0x7f) | 0x80) - dl never borrows across bytes.
+__device__ __forceinline__ uint32_t dissimilar4(uint32_t diff, uint32_t dl4, bool big) {
+  const uint32_t lo = ((diff & 0x7f7f7f7fu) | 0x80808080u) - dl4;
+  return (big ? (lo & diff) : (lo | diff)) & 0x80808080u;
 }
-// similar run going forward: byte o is the first neighbour
-__device__ __forceinline__ int run_fwd(const uint32_t* s32, int o, int lim, uint32_t c4, uint32_t d4) {
-  for (int n = 0; n < lim; n += 4) {
-    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(s32, o + n), c4), d4);
-    if (ge) return min(n + ((__ffs(ge) - 1) >> 3), lim);
+// Length of the similar run starting at byte offset o (the first neighbour)
+// and going up, capped at lim: aligned word loads, first dissimilar byte by ffs.
+__device__ __forceinline__ int run_fwd(const uint32_t* s32, int o, int lim, uint32_t c4,
+                                       uint32_t dl4, bool big) {
+  int w = o >> 2, first = -(o & 3);
+  uint32_t m = dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) & (0xffffffffu << (8 * (o & 3)));
+  for (;;) {
+    if (m) return min(first + ((__ffs(m) - 1) >> 3), lim);
+    first += 4;
+    if (first >= lim) return lim;
+    m = dissimilar4(__vabsdiffu4(s32[++w], c4), dl4, big);
   }
-  return lim;
 }
-// similar run going backward: byte o - 1 is the first neighbour
-__device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint32_t c4, uint32_t d4) {
-  for (int n = 0; n < lim; n += 4) {
-    const uint32_t ge = __vcmpgeu4(__vabsdiffu4(ld4u(s32, o - n - 4), c4), d4);
-    if (ge) return min(n + (__clz(ge) >> 3), lim);
+// Same going down from byte o - 1 (the first neighbour).
+__device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint32_t c4,
+                                       uint32_t dl4, bool big) {
+  int w = (o - 1) >> 2, top = (o - 1) & 3;
+  uint32_t m = dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) & (0xffffffffu >> (8 * (3 - top)));
+  for (;;) {
+    if (m) return min(top - ((31 - __clz(m)) >> 3), lim);
+    top += 4;
+    if (top - 3 >= lim) return lim;
+    m = dissimilar4(__vabsdiffu4(s32[--w], c4), dl4, big);
   }
-  return lim;
 }
 
 __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
@@ -159,13 +169,15 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     n = min(a.w_x, a.Ws - 1 - x); m = min(a.w_x, x);
     N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
   } else {
-    const uint32_t c4 = (uint32_t)c * 0x01010101u, d4 = (uint32_t)a.delta * 0x01010101u;
+    const bool big = a.delta >= 128;
+    const uint32_t c4 = (uint32_t)c * 0x01010101u;
+    const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
     const int oB = (ty + 2) * BWp + tx + HX + 8;                 // centre in sB
     const int oV = 12 * BWp + (tx + 2) * AHp + ty + HY + 8;      // centre in sV
-    n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, d4);
-    m = run_bwd(psm32, oB, min(a.w_x, x), c4, d4);
-    N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, d4);
-    M = run_bwd(psm32, oV, min(a.w_y, y), c4, d4);
+    n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, dl4, big);
+    m = run_bwd(psm32, oB, min(a.w_x, x), c4, dl4, big);
+    N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, dl4, big);
+    M = run_bwd(psm32, oV, min(a.w_y, y), c4, dl4, big);
   }
   const size_t o = (size_t)y * a.Ws + x;
   (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
@@ -230,18 +242,24 @@ constexpr int kXWarps = 8;
 constexpr int kXDPerUnit = 16;
 
 template <int C>
-__global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
+__global__ void __launch_bounds__(kXWarps * 32, 2) xpass_kernel(XArgs a) {
   extern __shared__ uint32_t xsm[];
-  uint32_t* sQAD = xsm;              // [256][32]
-  uint32_t* sQMC = sQAD + 256 * 32;  // [64][32], indexed by cL ^ cR
-  uint32_t* sL = sQMC + 64 * 32;     // [32C] pixL row (u32)
-  uint32_t* sR = sL + 32 * C;        // [32C] pixR row
-  uint32_t* sA = sR + 32 * C;        // [32C] mL | nL<<8 | mR<<16 | nR<<24
+  uint32_t* sQAD = xsm;              // [256][32]  Q_AD[|dI|], one copy per bank
+  uint32_t* sQMC = sQAD + 256 * 32;  // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
+  uint32_t* sL = sQMC + 64 * 32;     // [32C] left row:  census | I << 24
+  uint32_t* sR = sL + 32 * C;        // [32C] right row: census | I << 24
+  uint32_t* sAL = sR + 32 * C;       // [32C] byte offsets 4(x-m_L) | 4(x+n_L+1) << 16
+  uint32_t* sAR = sAL + 32 * C;      // [32C] byte offsets 4(x-m_R) | 4(x+n_R+1) << 16
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* P = sA + 32 * C + warp * a.PL;  // [PL] exclusive prefix (+ BORDER extension)
+  uint32_t* P = sAR + 32 * C + warp * a.PL;  // [PL] exclusive prefix (+ BORDER extension)
 
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sQAD[i] = __ldg(a.qad + (i >> 5));
   for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) sQMC[i] = __ldg(a.qmc + __popc(i >> 5));
+  // with pixels encoded as census | I << 24, |dI|*128 = vabsdiffu4(pl, pr) >> 17 and
+  // (cL ^ cR)*128 = ((pl ^ pr) & 63) << 7: table addresses in two ALU operations.
+  const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
+  const char* qmcb = reinterpret_cast<const char*>(sQMC + lane);
+  const char* Pb = reinterpret_cast<const char*>(P);
 
   const int nch = (a.Ds + kXDPerUnit - 1) / kXDPerUnit;
   const int units = a.Hs * nch;
@@ -251,14 +269,17 @@ __global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
     const int y = u / nch, d0 = (u - y * nch) * kXDPerUnit;
     __syncthreads();  // previous unit finished with the row buffers
     for (int x = threadIdx.x; x < 32 * C; x += blockDim.x) {
-      uint32_t l = 0, r = 0, ar = 0;
+      uint32_t l = 0, r = 0, al = 4u * x | (4u * (x + 1)) << 16, ar = al;
       if (x < Ws) {
         const size_t o = (size_t)y * Ws + x;
-        l = __ldg(a.pixL + o);
-        r = __ldg(a.pixR + o);
-        ar = (__ldg(a.armL + o) & 0xffffu) | (__ldg(a.armR + o) << 16);
+        const uint32_t pl = __ldg(a.pixL + o), pr = __ldg(a.pixR + o);
+        l = (pl >> 8) | (pl << 24);
+        r = (pr >> 8) | (pr << 24);
+        const uint32_t aL = __ldg(a.armL + o), aR = __ldg(a.armR + o);
+        al = 4u * (x - (aL & 255u)) | (4u * (x + ((aL >> 8) & 255u) + 1)) << 16;
+        ar = 4u * (x - (aR & 255u)) | (4u * (x + ((aR >> 8) & 255u) + 1)) << 16;
       }
-      sL[x] = l; sR[x] = r; sA[x] = ar;
+      sL[x] = l; sR[x] = r; sAL[x] = al; sAR[x] = ar;
     }
     __syncthreads();
 #pragma unroll 1
@@ -274,11 +295,9 @@ __global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
 #pragma unroll
       for (int k = 0; k < C; ++k) {
         const uint32_t pl = Lr[k], pr = Rr[k];
-        const uint32_t ad = __vabsdiffu4(pl, pr) & 255u;
-        const uint32_t hx = ((pl ^ pr) >> 8) & 63u;
-        uint32_t q = sQAD[(ad << 5) | lane] + sQMC[(hx << 5) | lane];
-        q = (k < nb) ? border : q;  // reading R12b: out of the right image
-        run += q;
+        const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
+        const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & 63u) << 7));
+        run += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
         pref[k] = run;
       }
       uint32_t incl = run;
@@ -296,20 +315,19 @@ __global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
       const uint32_t PW = P[Ws];
       for (int e = lane; e < a.ext; e += 32) P[Ws + 1 + e] = PW + (uint32_t)(e + 1) * border;
       __syncwarp();
-      // ---- phase C: window differences, coalesced stores
-      uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp;
-      uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp;
-      const uint32_t* Pd = P + d;
+      // ---- phase C: window differences (precomputed byte offsets), coalesced stores
+      uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp + lane;
+      uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp + lane;
+      const char* Pdb = Pb + 4 * d;
 #pragma unroll
       for (int i = 0; i < C; ++i) {
-        const int x = lane + 32 * i;
-        const uint32_t ar = sA[x];
-        const uint32_t caL = P[x + ((ar >> 8) & 255u) + 1] - P[x - (int)(ar & 255u)];
-        const uint32_t caR = Pd[x + (ar >> 24) + 1] - Pd[x - (int)((ar >> 16) & 255u)];
-        if (x < Ws) {
-          outL[x] = caL;
-          outR[x] = caR;
-        }
+        const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
+        const uint32_t caL = *reinterpret_cast<const uint32_t*>(Pb + (al >> 16)) -
+                             *reinterpret_cast<const uint32_t*>(Pb + (al & 0xffffu));
+        const uint32_t caR = *reinterpret_cast<const uint32_t*>(Pdb + (ar >> 16)) -
+                             *reinterpret_cast<const uint32_t*>(Pdb + (ar & 0xffffu));
+        outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
+        outR[32 * i] = caR;
       }
       __syncwarp();
     }
@@ -317,8 +335,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 3) xpass_kernel(XArgs a) {
 }
 
 int xpass_chunk_for(int Ws) {
-  static const int cs[] = {3, 7, 15, 23, 31, 47, 63};
-  for (int c : cs)
+  for (int c = 3; c <= 63; c += 2)
     if (32 * c >= Ws) return c;
   return 0;
 }
@@ -345,13 +362,37 @@ static int occ_xpass_c(int smem) {
 
 #define XPASS_DISPATCH(C_, EXPR)                        \
   switch (C_) {                                         \
-    case 3: { constexpr int CC = 3; EXPR; } break;      \
-    case 7: { constexpr int CC = 7; EXPR; } break;      \
-    case 15: { constexpr int CC = 15; EXPR; } break;    \
-    case 23: { constexpr int CC = 23; EXPR; } break;    \
-    case 31: { constexpr int CC = 31; EXPR; } break;    \
-    case 47: { constexpr int CC = 47; EXPR; } break;    \
-    case 63: { constexpr int CC = 63; EXPR; } break;    \
+    case 3: { constexpr int CC = 3; EXPR; } break;   \
+    case 5: { constexpr int CC = 5; EXPR; } break;   \
+    case 7: { constexpr int CC = 7; EXPR; } break;   \
+    case 9: { constexpr int CC = 9; EXPR; } break;   \
+    case 11: { constexpr int CC = 11; EXPR; } break;   \
+    case 13: { constexpr int CC = 13; EXPR; } break;   \
+    case 15: { constexpr int CC = 15; EXPR; } break;   \
+    case 17: { constexpr int CC = 17; EXPR; } break;   \
+    case 19: { constexpr int CC = 19; EXPR; } break;   \
+    case 21: { constexpr int CC = 21; EXPR; } break;   \
+    case 23: { constexpr int CC = 23; EXPR; } break;   \
+    case 25: { constexpr int CC = 25; EXPR; } break;   \
+    case 27: { constexpr int CC = 27; EXPR; } break;   \
+    case 29: { constexpr int CC = 29; EXPR; } break;   \
+    case 31: { constexpr int CC = 31; EXPR; } break;   \
+    case 33: { constexpr int CC = 33; EXPR; } break;   \
+    case 35: { constexpr int CC = 35; EXPR; } break;   \
+    case 37: { constexpr int CC = 37; EXPR; } break;   \
+    case 39: { constexpr int CC = 39; EXPR; } break;   \
+    case 41: { constexpr int CC = 41; EXPR; } break;   \
+    case 43: { constexpr int CC = 43; EXPR; } break;   \
+    case 45: { constexpr int CC = 45; EXPR; } break;   \
+    case 47: { constexpr int CC = 47; EXPR; } break;   \
+    case 49: { constexpr int CC = 49; EXPR; } break;   \
+    case 51: { constexpr int CC = 51; EXPR; } break;   \
+    case 53: { constexpr int CC = 53; EXPR; } break;   \
+    case 55: { constexpr int CC = 55; EXPR; } break;   \
+    case 57: { constexpr int CC = 57; EXPR; } break;   \
+    case 59: { constexpr int CC = 59; EXPR; } break;   \
+    case 61: { constexpr int CC = 61; EXPR; } break;   \
+    case 63: { constexpr int CC = 63; EXPR; } break;   \
     default: break;                                     \
   }
 
@@ -589,6 +630,7 @@ struct PostArgs {
   unsigned* counter;
   int W, H, Ws, Hs, K, T;
   int Wsp;  // Ws rounded up to 32
+  int Wx;   // W rounded up to 4
 };
 
 __device__ __forceinline__ void cswap(int& a, int& b) {
@@ -664,73 +706,83 @@ __device__ void su_row_global(const PostArgs& a, int Y, float thr) {
   }
 }
 
+constexpr int kPostRows = 2;  // scaled rows owned per CTA
+
 __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
   extern __shared__ uint32_t psm_[];
-  const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5;
-  uint8_t* mk = reinterpret_cast<uint8_t*>(psm_);                // [4][Wsp] masked rows y-1..y+2
-  uint8_t* md = mk + 4 * Wsp;                                    // [2][Wsp] median rows y, y+1
-  float* fv = reinterpret_cast<float*>(md + 2 * Wsp);            // [2][Wsp] fill rows y, y+1
-  uint32_t* cmask = reinterpret_cast<uint32_t*>(fv + 2 * Wsp);   // [2][64]
-  int* prevLast = reinterpret_cast<int*>(cmask + 128);           // [2][64]
-  int* nextFirst = prevLast + 128;                               // [2][64]
+  constexpr int R = kPostRows;
+  const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5, W = a.W, Wx = a.Wx;
+  uint8_t* mk = reinterpret_cast<uint8_t*>(psm_);                  // [R+3][Wsp] masked rows
+  uint8_t* md = mk + (R + 3) * Wsp;                                // [R+1][Wsp] median rows
+  float* fv = reinterpret_cast<float*>(md + (R + 1) * Wsp);        // [R+1][Wsp] fill rows
+  float* xr = fv + (R + 1) * Wsp;                                  // [R+1][Wx]  x-filled rows (K=2)
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(xr + (R + 1) * Wx); // [R+1][64]
+  int* prevLast = reinterpret_cast<int*>(cmask + (R + 1) * 64);    // [R+1][64]
+  int* nextFirst = prevLast + (R + 1) * 64;                        // [R+1][64]
   __shared__ int s_last;
-  const int y = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nrows = (a.K == 2 && y + 1 < a.Hs) ? 2 : 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int y0 = blockIdx.x * R;
+  const int nr = min(R, a.Hs - y0);                          // owned scaled rows
+  const int nf = a.K == 2 ? min(nr + 1, a.Hs - y0) : nr;     // fill rows needed (SU reads y+1)
   const float thr = (float)(a.K * a.T);
 
-  // 1. masked rows y-1 .. y+nrows (clamped rows, Eq. 10)
-  for (int i = tid; i < (nrows + 2) * Ws; i += blockDim.x) {
-    const int r = i / Ws, x = i - r * Ws;
-    const int yy = clampi(y - 1 + r, 0, a.Hs - 1);
-    const int k = __ldg(a.DL + (size_t)yy * Ws + x);
-    const bool gcp = (x - k >= 0) && (__ldg(a.DR + (size_t)yy * Ws + x - k) == k);
-    mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+  // 1. masked rows y0-1 .. y0+nf (clamped), Eq. 10
+  for (int r = 0; r < nf + 2; ++r) {
+    const int yy = clampi(y0 - 1 + r, 0, a.Hs - 1);
+    const uint8_t* dl = a.DL + (size_t)yy * Ws;
+    const uint8_t* dr = a.DR + (size_t)yy * Ws;
+    for (int x = tid; x < Ws; x += blockDim.x) {
+      const int k = __ldg(dl + x);
+      const bool gcp = (x - k >= 0) && (__ldg(dr + x - k) == k);
+      mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+    }
   }
   __syncthreads();
-  // 2. median rows y, y+1
-  for (int i = tid; i < nrows * Ws; i += blockDim.x) {
-    const int j = i / Ws, x = i - j * Ws;
-    const int c = mk[(j + 1) * Wsp + x];
-    int out = kInvalid;
-    if (c != kInvalid) {
-      const int xl = max(x - 1, 0), xr = min(x + 1, Ws - 1);
-      const uint8_t* r0 = mk + j * Wsp;
-      const uint8_t* r1 = r0 + Wsp;
-      const uint8_t* r2 = r1 + Wsp;
-      int v0 = r0[xl], v1 = r0[x], v2 = r0[xr];
-      int v3 = r1[xl], v4 = c, v5 = r1[xr];
-      int v6 = r2[xl], v7 = r2[x], v8 = r2[xr];
-      const int n = (v0 != kInvalid) + (v1 != kInvalid) + (v2 != kInvalid) + (v3 != kInvalid) + 1 +
-                    (v5 != kInvalid) + (v6 != kInvalid) + (v7 != kInvalid) + (v8 != kInvalid);
-      cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
-      cswap(v1, v2); cswap(v4, v5); cswap(v7, v8);
-      cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
-      cswap(v0, v3); cswap(v3, v6); cswap(v0, v3);
-      cswap(v1, v4); cswap(v4, v7); cswap(v1, v4);
-      cswap(v2, v5); cswap(v5, v8); cswap(v2, v5);
-      cswap(v1, v3); cswap(v5, v7); cswap(v2, v6);
-      cswap(v4, v6); cswap(v2, v4); cswap(v2, v3);
-      cswap(v5, v6);
-      const int kk = (n - 1) >> 1;  // 0..4
-      out = kk == 0 ? v0 : kk == 1 ? v1 : kk == 2 ? v2 : kk == 3 ? v3 : v4;
-    }
-    md[j * Wsp + x] = (uint8_t)out;
-    if (j == 0) {
-      a.masked[(size_t)y * Ws + x] = (uint8_t)c;
-      a.median[(size_t)y * Ws + x] = (uint8_t)out;
+  // 2. median rows y0 .. y0+nf-1
+  for (int j = 0; j < nf; ++j) {
+    const uint8_t* r0 = mk + j * Wsp;
+    const uint8_t* r1 = r0 + Wsp;
+    const uint8_t* r2 = r1 + Wsp;
+    for (int x = tid; x < Ws; x += blockDim.x) {
+      const int c = r1[x];
+      int out = kInvalid;
+      if (c != kInvalid) {
+        const int xl = max(x - 1, 0), xr_ = min(x + 1, Ws - 1);
+        int v0 = r0[xl], v1 = r0[x], v2 = r0[xr_];
+        int v3 = r1[xl], v4 = c, v5 = r1[xr_];
+        int v6 = r2[xl], v7 = r2[x], v8 = r2[xr_];
+        const int n = (v0 != kInvalid) + (v1 != kInvalid) + (v2 != kInvalid) + (v3 != kInvalid) +
+                      1 + (v5 != kInvalid) + (v6 != kInvalid) + (v7 != kInvalid) + (v8 != kInvalid);
+        cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
+        cswap(v1, v2); cswap(v4, v5); cswap(v7, v8);
+        cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
+        cswap(v0, v3); cswap(v3, v6); cswap(v0, v3);
+        cswap(v1, v4); cswap(v4, v7); cswap(v1, v4);
+        cswap(v2, v5); cswap(v5, v8); cswap(v2, v5);
+        cswap(v1, v3); cswap(v5, v7); cswap(v2, v6);
+        cswap(v4, v6); cswap(v2, v4); cswap(v2, v3);
+        cswap(v5, v6);
+        const int kk = (n - 1) >> 1;  // 0..4
+        out = kk == 0 ? v0 : kk == 1 ? v1 : kk == 2 ? v2 : kk == 3 ? v3 : v4;
+      }
+      md[j * Wsp + x] = (uint8_t)out;
+      if (j < nr) {
+        a.masked[(size_t)(y0 + j) * Ws + x] = (uint8_t)c;
+        a.median[(size_t)(y0 + j) * Ws + x] = (uint8_t)out;
+      }
     }
   }
   __syncthreads();
   // 3. per-32-pixel validity masks
-  for (int c = warp; c < nrows * nch; c += blockDim.x >> 5) {
-    const int j = c / nch, cc = c - j * nch;
-    const int x = cc * 32 + lane;
-    const unsigned m = __ballot_sync(kFull, x < Ws && md[j * Wsp + x] != kInvalid);
-    if (lane == 0) cmask[j * 64 + cc] = m;
-  }
+  for (int j = 0; j < nf; ++j)
+    for (int cc = warp; cc < nch; cc += blockDim.x >> 5) {
+      const int x = cc * 32 + lane;
+      const unsigned m = __ballot_sync(kFull, x < Ws && md[j * Wsp + x] != kInvalid);
+      if (lane == 0) cmask[j * 64 + cc] = m;
+    }
   __syncthreads();
   // 4. warp j: exclusive max-scan of chunk last-valid, reverse min-scan of first-valid
-  if (warp < nrows) {
+  if (warp < nf) {
     const int j = warp;
     int carry = -1;
     for (int base = 0; base < nch; base += 32) {
@@ -745,7 +797,6 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
       if (cc < nch) prevLast[j * 64 + cc] = lane == 0 ? carry : max(carry, prev);
       carry = max(carry, __shfl_sync(kFull, v, 31));
     }
-    if (j == 0 && lane == 0) a.rowLast[y] = carry;
     int rc = INT_MAX;  // INT_MAX = none
     for (int base = ((nch - 1) >> 5) << 5; base >= 0; base -= 32) {
       const int cc = base + lane;
@@ -760,45 +811,81 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
       if (cc < nch) nextFirst[j * 64 + cc] = excl == INT_MAX ? -1 : excl;
       rc = min(rc, __shfl_sync(kFull, v, 0));
     }
-    if (j == 0 && lane == 0) a.rowFirst[y] = rc == INT_MAX ? -1 : rc;
+    if (j < nr && lane == 0) {
+      a.rowLast[y0 + j] = carry;
+      a.rowFirst[y0 + j] = rc == INT_MAX ? -1 : rc;
+    }
   }
   __syncthreads();
-  // 5. fill values of rows y, y+1
-  for (int i = tid; i < nrows * Wsp; i += blockDim.x) {
-    const int j = i / Wsp, x = i - j * Wsp;
-    if (x >= Ws) continue;
+  // 5. fill values of rows y0 .. y0+nf-1
+  for (int j = 0; j < nf; ++j) {
     const uint8_t* mdr = md + j * Wsp;
-    float v;
-    if (mdr[x] != kInvalid) {
-      v = (float)mdr[x];
-    } else {
-      const int cc = x >> 5, ln = x & 31;
-      const unsigned m = cmask[j * 64 + cc];
-      const unsigned below = m & ((1u << ln) - 1u);
-      const unsigned above = ln == 31 ? 0u : (m & ~((2u << ln) - 1u));
-      const int li = below ? cc * 32 + 31 - __clz(below) : prevLast[j * 64 + cc];
-      const int ri = above ? cc * 32 + __ffs(above) - 1 : nextFirst[j * 64 + cc];
-      v = fill_value(mdr, a.pixL + (size_t)(y + j) * Ws, x, li, ri, a.T);
-    }
-    fv[j * Wsp + x] = v;
-    if (j == 0) {
-      if (a.K == 2) a.fill[(size_t)y * Ws + x] = v;
-      else a.out[(size_t)y * Ws + x] = v;
+    const uint16_t* pix = a.pixL + (size_t)(y0 + j) * Ws;
+    for (int x = tid; x < Ws; x += blockDim.x) {
+      float v;
+      if (mdr[x] != kInvalid) {
+        v = (float)mdr[x];
+      } else {
+        const int cc = x >> 5, ln = x & 31;
+        const unsigned m = cmask[j * 64 + cc];
+        const unsigned below = m & ((1u << ln) - 1u);
+        const unsigned above = ln == 31 ? 0u : (m & ~((2u << ln) - 1u));
+        const int li = below ? cc * 32 + 31 - __clz(below) : prevLast[j * 64 + cc];
+        const int ri = above ? cc * 32 + __ffs(above) - 1 : nextFirst[j * 64 + cc];
+        v = fill_value(mdr, pix, x, li, ri, a.T);
+      }
+      fv[j * Wsp + x] = v;
+      if (j < nr) (a.K == 2 ? a.fill : a.out)[(size_t)(y0 + j) * Ws + x] = v;
     }
   }
   if (a.K == 2) {
     __syncthreads();
-    // 6. scale-up: output rows 2y, 2y+1 (+ the extra last row of an odd H)
-    const uint8_t* L0 = a.Lorg + (size_t)(2 * y) * a.W;
-    const uint8_t* L1 = a.Lorg + (size_t)(2 * min(y + 1, a.Hs - 1)) * a.W;
-    for (int X = tid; X < a.W; X += blockDim.x) {
-      const float v0 = su_xval(fv, L0, X, a.W, Ws, thr);
-      a.out[(size_t)(2 * y) * a.W + X] = v0;
-      if (2 * y + 1 < a.H) {
-        float v1 = v0;
-        if (nrows == 2) v1 = __fmul_rn(__fadd_rn(v0, su_xval(fv + Wsp, L1, X, a.W, Ws, thr)), 0.5f);
-        a.out[(size_t)(2 * y + 1) * a.W + X] = v1;
-        if (y == a.Hs - 1 && 2 * y + 2 < a.H) a.out[(size_t)(2 * y + 2) * a.W + X] = v1;
+    // 6a. x pass of Step8 on the seeded rows: xr[j][X] for X < W (pairs 2p, 2p+1)
+    for (int j = 0; j < nf; ++j) {
+      const float* f = fv + j * Wsp;
+      const uint8_t* L = a.Lorg + (size_t)(2 * (y0 + j)) * W;
+      float* o = xr + j * Wx;
+      for (int p = tid; 2 * p < W; p += blockDim.x) {
+        if (p < Ws) {
+          const float av = 2.0f * f[p];
+          o[2 * p] = av;
+          if (2 * p + 1 < W) {
+            float v = av;
+            if (p + 1 < Ws) {
+              const float bv = 2.0f * f[p + 1];
+              if (fabsf(__fsub_rn(av, bv)) <= thr) {
+                v = __fmul_rn(__fadd_rn(av, bv), 0.5f);
+              } else {
+                const int c = __ldg(L + 2 * p + 1);
+                v = (abs((int)__ldg(L + 2 * p) - c) <= abs((int)__ldg(L + 2 * p + 2) - c)) ? av : bv;
+              }
+            }
+            o[2 * p + 1] = v;
+          }
+        } else {  // odd W: the extra last column copies its predecessor (an odd column = av)
+          o[2 * p] = 2.0f * f[Ws - 1];
+        }
+      }
+    }
+    __syncthreads();
+    // 6b. output rows 2y, 2y+1 (+ the extra last row of an odd H): y pass, linear
+    for (int j = 0; j < nr; ++j) {
+      const int y = y0 + j;
+      const float* x0r = xr + j * Wx;
+      const float* x1r = xr + (j + 1) * Wx;
+      const bool down = j + 1 < nf;
+      float* o0 = a.out + (size_t)(2 * y) * W;
+      float* o1 = o0 + W;
+      const bool has1 = 2 * y + 1 < a.H;
+      const bool extra = (y == a.Hs - 1) && (2 * y + 2 < a.H);
+      for (int X = tid; X < W; X += blockDim.x) {
+        const float v0 = x0r[X];
+        o0[X] = v0;
+        if (has1) {
+          const float v1 = down ? __fmul_rn(__fadd_rn(v0, x1r[X]), 0.5f) : v0;
+          o1[X] = v1;
+          if (extra) o1[W + X] = v1;
+        }
       }
     }
   }
@@ -842,7 +929,8 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.Wsp = (g.Ws + 31) & ~31;
-  post_kernel<<<g.Hs, 256, p.post_smem, s>>>(a);
+  a.Wx = (g.W + 3) & ~3;
+  post_kernel<<<(g.Hs + kPostRows - 1) / kPostRows, 256, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -887,7 +975,12 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     p.prep_smem = 12 * BWp + 36 * AHp + 16;
   }
   const int Wsp = (g.Ws + 31) & ~31;
-  p.post_smem = 4 * Wsp + 2 * Wsp + 2 * Wsp * 4 + 3 * 128 * 4 + 64;
+  const int Wx = (g.W + 3) & ~3;
+  p.post_smem = (kPostRows + 3) * Wsp + (kPostRows + 1) * Wsp + (kPostRows + 1) * Wsp * 4 +
+                (kPostRows + 1) * Wx * 4 + 3 * (kPostRows + 1) * 64 * 4 + 64;
+  if (p.post_smem > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
+    return e;
   if (p.sd_smem > 48 * 1024) {
     switch (g.m_pool) {
       case 0: e = cudaFuncSetAttribute(sd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
@@ -901,7 +994,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
   p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x + 3;
-  p.xpass_smem = (int)(sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + 3 * 32 * p.xpass_C +
+  p.xpass_smem = (int)(sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + 4 * 32 * p.xpass_C +
                                            (size_t)kXWarps * p.xpass_PL));
   int occ = 0;
   XPASS_DISPATCH(p.xpass_C, (e = setup_xpass_c<CC>(p.xpass_smem), occ = occ_xpass_c<CC>(p.xpass_smem)));
