@@ -149,13 +149,15 @@ int stereo_get_tables(const stereo_t* h, uint32_t* qad, uint32_t* qmc, uint32_t*
  *   STEREO_BUF_MASKED  : u8  [Hs][Ws]  D^L with non-GCPs = 255 (Eq. 10)
  *   STEREO_BUF_MEDIAN  : u8  [Hs][Ws]  after the 3x3 median
  *   STEREO_BUF_FILL    : f32 [Hs][Ws]  D^{+L}
+ *   STEREO_BUF_ROWS    : i32 [4][Hs]   per median-map row: first valid x, last
+ *                        valid x, value at first, value at last (-1 = none)
  * stereo_debug_download synchronises the device; `bytes` must equal the
  * buffer size exactly (STEREO_EINVAL otherwise). */
 enum {
   STEREO_BUF_PIX_L = 0, STEREO_BUF_PIX_R, STEREO_BUF_ARM_L, STEREO_BUF_ARM_R,
   STEREO_BUF_CAX_L, STEREO_BUF_CAX_R, STEREO_BUF_CA_L, STEREO_BUF_CA_R,
   STEREO_BUF_DL, STEREO_BUF_DR, STEREO_BUF_MASKED, STEREO_BUF_MEDIAN,
-  STEREO_BUF_FILL, STEREO_BUF_COUNT
+  STEREO_BUF_FILL, STEREO_BUF_ROWS, STEREO_BUF_COUNT
 };
 int stereo_debug_download(stereo_t* h, int buf_id, void* host_dst, size_t bytes);
 int stereo_debug_upload(stereo_t* h, int buf_id, const void* host_src, size_t bytes);
@@ -179,6 +181,18 @@ enum {
 };
 int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,
                      float* disp_out, void* stream);
+
+/* Row-band support.  A band of a frame is computed by running
+ * the normal pipeline on a sub-image whose halo rows cover the dependency cone
+ * of the band's own rows; only rule (d) of the fill (a row without any valid
+ * pixel takes the nearest valid value in raster order, which may lie in
+ * another band) needs global information.  stereo_patch_rows sets the listed
+ * scaled rows (HOST int32 rows[n], band-local) of D^{+L} to the HOST values[n]
+ * and recomputes the scale-up rows that read them into disp_out (DEVICE, the
+ * band's f32 output); L is the band's DEVICE original left image (K = 2).
+ * Synchronises `stream` before returning. */
+int stereo_patch_rows(stereo_t* h, const int32_t* rows, const float* values, int n,
+                      const uint8_t* L, float* disp_out, void* stream);
 
 /* Per-stage device timing with CUDA events recorded on the compute stream.
  * stereo_set_timing(h, 1) resets the accumulators and starts recording around

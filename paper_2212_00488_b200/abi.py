@@ -24,7 +24,7 @@ STEREO_ABI_VERSION = 1
 STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, -1, -2, -3, -4
 
 (BUF_PIX_L, BUF_PIX_R, BUF_ARM_L, BUF_ARM_R, BUF_CAX_L, BUF_CAX_R, BUF_CA_L, BUF_CA_R,
- BUF_DL, BUF_DR, BUF_MASKED, BUF_MEDIAN, BUF_FILL) = range(13)
+ BUF_DL, BUF_DR, BUF_MASKED, BUF_MEDIAN, BUF_FILL, BUF_ROWS) = range(14)
 (STAGE_SD, STAGE_PREP, STAGE_XPASS, STAGE_YPASS, STAGE_POST) = range(5)
 STAGE_NAMES = ("SD", "PREP", "XPASS", "YPASS", "POST")
 STAGE_COUNT = 5
@@ -35,7 +35,7 @@ EXPORTS = (
     "stereo_default_params", "stereo_create", "stereo_compute", "stereo_compute_batch",
     "stereo_compute_host", "stereo_destroy", "stereo_last_error", "stereo_get_info",
     "stereo_get_tables", "stereo_debug_download", "stereo_debug_upload", "stereo_set_debug",
-    "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms",
+    "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms", "stereo_patch_rows",
 )
 
 
@@ -104,6 +104,7 @@ def lib():
             "stereo_run_stage": (i32, [vp, i32, vp, vp, vp, vp]),
             "stereo_set_timing": (i32, [vp, i32]),
             "stereo_stage_times_ms": (i32, [vp, vp, C.POINTER(C.c_int)]),
+            "stereo_patch_rows": (i32, [vp, vp, vp, i32, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -220,6 +221,7 @@ class Stereo:
             BUF_CA_L: ((i.Ds, i.Hs, i.Ws), np.uint64), BUF_CA_R: ((i.Ds, i.Hs, i.Ws), np.uint64),
             BUF_DL: (n2, np.uint8), BUF_DR: (n2, np.uint8), BUF_MASKED: (n2, np.uint8),
             BUF_MEDIAN: (n2, np.uint8), BUF_FILL: (n2, np.float32),
+            BUF_ROWS: ((4, i.Hs), np.int32),
         }[buf]
 
     def download(self, buf):
@@ -239,6 +241,12 @@ class Stereo:
     def run_stage(self, stage, L=None, R=None, out=None, stream=None):
         _check(lib().stereo_run_stage(self._h, stage, _ptr(L), _ptr(R), _ptr(out),
                                       _stream_ptr(stream)))
+
+    def patch_rows(self, rows, values, L, out, stream=None):
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        values = np.ascontiguousarray(values, dtype=np.float32)
+        _check(lib().stereo_patch_rows(self._h, rows.ctypes.data, values.ctypes.data, len(rows),
+                                       _ptr(L), _ptr(out), _stream_ptr(stream)))
 
     def set_timing(self, enable=True):
         _check(lib().stereo_set_timing(self._h, int(enable)))

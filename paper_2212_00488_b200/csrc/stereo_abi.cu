@@ -216,6 +216,7 @@ BufView buf_view(stereo_t* h, int id) {
     case STEREO_BUF_MASKED: return {h->b.masked, n};
     case STEREO_BUF_MEDIAN: return {h->b.median, n};
     case STEREO_BUF_FILL: return {h->b.fill, n * 4};
+    case STEREO_BUF_ROWS: return {h->b.rowFirst, (size_t)g.Hs * 16};
     default: return {nullptr, 0};
   }
 }
@@ -283,7 +284,8 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       {(void**)&b.pixL, n * 2}, {(void**)&b.pixR, n * 2}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
       {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
-      {(void**)&b.rowFirst, (size_t)g.Hs * 4}, {(void**)&b.rowLast, (size_t)g.Hs * 4},
+      {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
+      {(void**)&b.patchVals, (size_t)g.Hs * 4},
       {(void**)&b.counter, 16},
       {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
   };
@@ -296,6 +298,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       return rc;
     }
   }
+  b.rowLast = b.rowFirst + g.Hs;
   e = cudaMemset(b.counter, 0, 16);
   if (e == cudaSuccess) e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(b.qmc, h->qmc_h, sizeof h->qmc_h, cudaMemcpyHostToDevice);
@@ -445,6 +448,22 @@ int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t*
       return STEREO_OK;
     default: return fail(STEREO_EINVAL, "unknown stage %d", stage_id);
   }
+}
+
+int stereo_patch_rows(stereo_t* h, const int32_t* rows, const float* values, int n,
+                      const uint8_t* L, float* disp_out, void* stream) {
+  if (!h || n < 0 || (n > 0 && (!rows || !values || !disp_out)) || (h->g.K == 2 && n > 0 && !L))
+    return fail(STEREO_EINVAL, "invalid patch arguments");
+  if (n > h->g.Hs) return fail(STEREO_EINVAL, "more rows than the handle has");
+  for (int i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] >= h->g.Hs) return fail(STEREO_EINVAL, "patch row %d out of range", rows[i]);
+  if (n == 0) return STEREO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(h->b.patchRows, rows, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h->b.patchVals, values, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+  CU(launch_patch(h->g, h->b, L, disp_out, h->b.patchRows, h->b.patchVals, n, s));
+  CU(cudaStreamSynchronize(s));  // rows/values are caller-owned host memory
+  return STEREO_OK;
 }
 
 int stereo_set_timing(stereo_t* h, int enable) {

@@ -37,8 +37,10 @@ struct Buffers {
   uint8_t* DR = nullptr;
   uint8_t* masked = nullptr;
   uint8_t* median = nullptr;
-  int32_t* rowFirst = nullptr;  // first valid x of the median map per row (or -1)
-  int32_t* rowLast = nullptr;   // last valid x (or -1)
+  int32_t* rowFirst = nullptr;  // int32 [4][Hs]: first valid x, last valid x, their values (-1 = none)
+  int32_t* rowLast = nullptr;   // = rowFirst + Hs
+  int32_t* patchRows = nullptr; // rule-(d) patch scratch: int32 [Hs] rows + f32 [Hs] values
+  float* patchVals = nullptr;
   unsigned* counter = nullptr;  // POST last-block counter (self-resetting)
   float* fill = nullptr;        // f32 [Hs][Ws]
   uint32_t* qad = nullptr;      // u32 [256]
@@ -75,6 +77,8 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
                          cudaStream_t s);
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
                         float* out, cudaStream_t s);
+cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,
+                         const int32_t* rows_dev, const float* vals_dev, int n, cudaStream_t s);
 
 // Plan helpers
 int xpass_chunk_for(int Ws);  // 0 if unsupported

@@ -811,9 +811,12 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
       if (cc < nch) nextFirst[j * 64 + cc] = excl == INT_MAX ? -1 : excl;
       rc = min(rc, __shfl_sync(kFull, v, 0));
     }
-    if (j < nr && lane == 0) {
-      a.rowLast[y0 + j] = carry;
-      a.rowFirst[y0 + j] = rc == INT_MAX ? -1 : rc;
+    if (j < nr && lane == 0) {  // per-row summary [first x, last x, first value, last value]
+      const int y = y0 + j, first = rc == INT_MAX ? -1 : rc;
+      a.rowLast[y] = carry;
+      a.rowFirst[y] = first;
+      a.rowFirst[2 * a.Hs + y] = first >= 0 ? md[j * Wsp + first] : -1;
+      a.rowFirst[3 * a.Hs + y] = carry >= 0 ? md[j * Wsp + carry] : -1;
     }
   }
   __syncthreads();
@@ -919,6 +922,35 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
     }
   }
   if (tid == 0) *a.counter = 0u;
+}
+
+// Rule (d) patch for band mode: rows whose value only global information fixes
+// (dist.py exchanges the per-row summaries).  One CTA: set the rows, then redo
+// Step8 for the output rows that read them.
+__global__ void __launch_bounds__(256) patch_kernel(PostArgs a, const int32_t* rows,
+                                                    const float* vals, int n) {
+  for (int i = 0; i < n; ++i) {
+    float* dst = (a.K == 2 ? a.fill : a.out) + (size_t)rows[i] * a.Ws;
+    for (int x = threadIdx.x; x < a.Ws; x += blockDim.x) dst[x] = vals[i];
+  }
+  __syncthreads();
+  if (a.K != 2) return;
+  const float thr = (float)(a.K * a.T);
+  for (int i = 0; i < n; ++i)
+    for (int Y = max(2 * rows[i] - 1, 0); Y <= min(2 * rows[i] + 2, a.H - 1); ++Y) su_row_global(a, Y, thr);
+}
+
+cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,
+                         const int32_t* rows_dev, const float* vals_dev, int n, cudaStream_t s) {
+  PostArgs a;
+  a.DL = b.DL; a.DR = b.DR; a.pixL = b.pixL; a.Lorg = Lorg;
+  a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
+  a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
+  a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
+  a.Wsp = (g.Ws + 31) & ~31;
+  a.Wx = (g.W + 3) & ~3;
+  patch_kernel<<<1, 256, 0, s>>>(a, rows_dev, vals_dev, n);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
