@@ -209,37 +209,58 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-    st = abi.Stereo(W, H, D)
+    NS = max(1, args.streams)
+    handles = [abi.Stereo(W, H, D) for _ in range(NS)]  # one handle per stream (not re-entrant)
+    st = handles[0]
     info = st.info
     frames = _frames(POOL, seed=1000 + rank)
     Lp = torch.from_numpy(np.stack([f[0] for f in frames])).to(dev)
     Rp = torch.from_numpy(np.stack([f[1] for f in frames])).to(dev)
-    out = torch.empty((2, H, W), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    out = torch.empty((NS, H, W), dtype=torch.float32, device=dev)
+    main = torch.cuda.current_stream(dev)
+    streams = [main] + [torch.cuda.Stream(dev) for _ in range(NS - 1)]
 
     def barrier():
         if ws > 1:
             dist.barrier()
 
-    def step(i):
-        st.compute(Lp[i % POOL], Rp[i % POOL], out[i & 1], stream=stream)
+    def step(i, ns=NS):
+        k = i % ns
+        handles[k].compute(Lp[i % POOL], Rp[i % POOL], out[k], stream=streams[k])
+
+    def timed(nsteps, ns):
+        """Device time of nsteps frames round-robin over ns streams (events on
+        the main stream; the other streams are forked from / joined into it)."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event() for _ in range(ns)]
+        e0.record(main)
+        for s_ in streams[1:ns]:
+            s_.wait_event(e0)
+        for i in range(nsteps):
+            step(args.warmup + i, ns)
+        for k in range(1, ns):
+            ends[k].record(streams[k])
+            main.wait_event(ends[k])
+        e1.record(main)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    ms_single = timed(min(args.steps, 500), 1) / min(args.steps, 500)  # one stream, for reference
     barrier()
     torch.cuda.synchronize()
-    st.set_timing(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms_total = timed(args.steps, NS)
     barrier()
     torch.cuda.synchronize()
-    ms_total = e0.elapsed_time(e1)
+    # per-kernel device time for the roofline: CUDA events recorded around every
+    # stage on the launch stream, over a second timed pass of the same frames
+    st.set_timing(True)
+    for i in range(min(args.steps, 512)):
+        step(args.warmup + i, 1)  # one stream: per-kernel times without overlap
+    torch.cuda.synchronize()
     stage_ms, nfr = st.stage_times_ms()
     st.set_timing(False)
     t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
@@ -251,27 +272,27 @@ def run_ours(args):
     # ---- end to end through the public C ABI with HOST buffers (pinned):
     # H2D of L, R + compute + D2H of the disparity map, every step, two
     # streams / two handles so copies overlap the previous frame's kernels.
-    st2 = abi.Stereo(W, H, D)
-    handles = (st, st2)
-    streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    st2 = abi.Stereo(W, H, D) if NS < 2 else handles[1]
+    e2e_h = (st, st2)
+    e2e_s = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     nh = 8
     Lh = [torch.from_numpy(frames[i][0]).pin_memory() for i in range(nh)]
     Rh = [torch.from_numpy(frames[i][1]).pin_memory() for i in range(nh)]
     Oh = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in range(nh)]
     e2e_steps = max(args.steps // 4, 8)
     for i in range(4):
-        handles[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=streams[i & 1])
+        e2e_h[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i & 1])
     torch.cuda.synchronize()
     barrier()
     ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     t0 = time.perf_counter()
     for s_ in range(2):
-        ea[s_].record(streams[s_])
+        ea[s_].record(e2e_s[s_])
     for i in range(e2e_steps):
-        handles[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=streams[i & 1])
+        e2e_h[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i & 1])
     for s_ in range(2):
-        eb[s_].record(streams[s_])
+        eb[s_].record(e2e_s[s_])
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     e2e_ms = max(ea[0].elapsed_time(eb[0]), ea[1].elapsed_time(eb[1]),
@@ -280,7 +301,8 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_fps = ws * e2e_steps / (float(t2.item()) / 1e3)
-    st2.close()
+    if NS < 2:
+        st2.close()
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -313,7 +335,9 @@ def run_ours(args):
                        "l2": f"inputs larger than L2: {POOL}-frame pool "
                              f"({POOL * W * H * 2 / 1e6:.0f} MB) + {2 * vol / 1e6:.0f} MB CA_x "
                              "written and read per frame",
-                       "parallelism": f"frame-batch dp{ws}" if ws > 1 else "single GPU"},
+                       "parallelism": f"frame-batch dp{ws}" if ws > 1 else "single GPU",
+                       "streams_per_gpu": NS,
+                       "ms_per_step_single_stream": ms_single},
             "gdisp_evals_per_s": fps * W * H * D / 1e9,
             "executed_gdisp_evals_per_s": fps * 2 * info.Ws * info.Hs * info.Ds / 1e9,
             "stage_us": {k: v / max(nfr, 1) * 1e3 for k, v in stage_ms.items()},
@@ -330,7 +354,8 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
-    st.close()
+    for h_ in handles:
+        h_.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -342,6 +367,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="frames in flight per GPU (one handle per stream)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -476,6 +476,12 @@ int stereo_set_timing(stereo_t* h, int enable) {
   for (double& v : h->acc_ms) v = 0;
   h->acc_frames = 0;
   h->timing = enable != 0;
+  // pre-create the events of ~512 frames so the timed loop never calls cudaEventCreate
+  while (h->timing && h->pool.size() < 512 * (STEREO_STAGE_COUNT + 1)) {
+    cudaEvent_t e = nullptr;
+    CU(cudaEventCreate(&e));
+    h->pool.push_back(e);
+  }
   return STEREO_OK;
 }
 

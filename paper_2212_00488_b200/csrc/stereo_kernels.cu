@@ -112,28 +112,37 @@ __device__ __forceinline__ uint32_t dissimilar4(uint32_t diff, uint32_t dl4, boo
   return (big ? (lo & diff) : (lo | diff)) & 0x80808080u;
 }
 // Length of the similar run starting at byte offset o (the first neighbour)
-// and going up, capped at lim: aligned word loads, first dissimilar byte by ffs.
+// and going up, capped at lim: aligned 8-byte steps, first dissimilar byte by
+// ffs on the 64-bit mask.
 __device__ __forceinline__ int run_fwd(const uint32_t* s32, int o, int lim, uint32_t c4,
                                        uint32_t dl4, bool big) {
   int w = o >> 2, first = -(o & 3);
-  uint32_t m = dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) & (0xffffffffu << (8 * (o & 3)));
+  const uint64_t keep = ~0ull << (8 * (o & 3));  // ignore bytes before o
+  uint64_t m = ((uint64_t)dissimilar4(__vabsdiffu4(s32[w + 1], c4), dl4, big) << 32 |
+                dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big)) & keep;
   for (;;) {
-    if (m) return min(first + ((__ffs(m) - 1) >> 3), lim);
-    first += 4;
+    if (m) return min(first + ((__ffsll((long long)m) - 1) >> 3), lim);
+    first += 8;
     if (first >= lim) return lim;
-    m = dissimilar4(__vabsdiffu4(s32[++w], c4), dl4, big);
+    w += 2;
+    m = (uint64_t)dissimilar4(__vabsdiffu4(s32[w + 1], c4), dl4, big) << 32 |
+        dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big);
   }
 }
 // Same going down from byte o - 1 (the first neighbour).
 __device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint32_t c4,
                                        uint32_t dl4, bool big) {
-  int w = (o - 1) >> 2, top = (o - 1) & 3;
-  uint32_t m = dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) & (0xffffffffu >> (8 * (3 - top)));
+  int w = (o - 1) >> 2, top = ((o - 1) & 3) + 4;  // distance of byte 0 of word w-1
+  const uint64_t keep = ~0ull >> (8 * (3 - ((o - 1) & 3)));  // ignore bytes above o-1
+  uint64_t m = ((uint64_t)dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) << 32 |
+                dissimilar4(__vabsdiffu4(s32[w - 1], c4), dl4, big)) & keep;
   for (;;) {
-    if (m) return min(top - ((31 - __clz(m)) >> 3), lim);
-    top += 4;
-    if (top - 3 >= lim) return lim;
-    m = dissimilar4(__vabsdiffu4(s32[--w], c4), dl4, big);
+    if (m) return min(top - ((63 - __clzll((long long)m)) >> 3), lim);
+    top += 8;
+    if (top - 7 >= lim) return lim;
+    w -= 2;
+    m = (uint64_t)dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) << 32 |
+        dissimilar4(__vabsdiffu4(s32[w - 1], c4), dl4, big);
   }
 }
 
@@ -149,12 +158,17 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws;
     for (int c = tx; c < BWp; c += 32) sB[r * BWp + c] = __ldg(row + clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
   }
-  // transposed vertical strip: lane = image row (coalescing is irrelevant here,
-  // the rows are L1/L2 resident) so the shared stores are bank-conflict free
-  for (int c = ty; c < 36; c += 8) {
-    const uint8_t* col = img + clampi(x0 - 2 + c, 0, a.Ws - 1);
-    for (int r = tx; r < AHp; r += 32)
-      sV[c * AHp + r] = __ldg(col + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws);
+  // vertical strip, stored transposed (column-major, odd word pitch AHp/4 so
+  // the transposing byte stores of a warp hit distinct banks); loaded row by
+  // row: lane = column, the row pointer is computed once per row
+  {
+    const int c0 = clampi(x0 - 2 + tx, 0, a.Ws - 1);
+    const int c1 = clampi(x0 + 30 + tx, 0, a.Ws - 1);  // columns 32..35 (tx < 4)
+    for (int r = ty; r < AHp; r += 8) {
+      const uint8_t* row = img + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws;
+      sV[tx * AHp + r] = __ldg(row + c0);
+      if (tx < 4) sV[(32 + tx) * AHp + r] = __ldg(row + c1);
+    }
   }
   __syncthreads();
   const int x = x0 + tx, y = y0 + ty;
@@ -189,7 +203,8 @@ static void prep_geometry(const Geom& g, int& HX, int& HY, int& BWp, int& AHp) {
   HX = g.w_x > 2 ? g.w_x : 2;
   HY = g.w_y > 2 ? g.w_y : 2;
   BWp = (32 + 2 * HX + 16 + 15) & ~15;
-  AHp = (8 + 2 * HY + 16 + 15) & ~15;
+  AHp = (8 + 2 * HY + 16 + 3) & ~3;
+  if (((AHp >> 2) & 1) == 0) AHp += 4;  // odd word pitch: conflict-free transposed stores
 }
 
 cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
@@ -657,13 +672,13 @@ __device__ __forceinline__ float su_xval(const float* f, const uint8_t* __restri
 }
 
 // bilateral fill value of pixel x given its nearest valid neighbours li / ri
-__device__ __forceinline__ float fill_value(const uint8_t* md, const uint16_t* __restrict__ pix,
+__device__ __forceinline__ float fill_value(const uint8_t* md, const uint16_t* pix,
                                             int x, int li, int ri, int T) {
   if (li >= 0 && ri >= 0) {
     const int Dl = md[li], Dr = md[ri];
     const int i = x - li, j = ri - x;
     if (abs(Dl - Dr) <= T) return __fdiv_rn((float)(Dl * j + Dr * i), (float)(i + j));
-    const int cI = __ldg(pix + x) & 255, lI = __ldg(pix + li) & 255, rI = __ldg(pix + ri) & 255;
+    const int cI = pix[x] & 255, lI = pix[li] & 255, rI = pix[ri] & 255;
     return (abs(lI - cI) <= abs(rI - cI)) ? (float)Dl : (float)Dr;
   }
   if (li >= 0) return (float)md[li];
@@ -708,7 +723,7 @@ __device__ void su_row_global(const PostArgs& a, int Y, float thr) {
 
 constexpr int kPostRows = 2;  // scaled rows owned per CTA
 
-__global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
+__global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   extern __shared__ uint32_t psm_[];
   constexpr int R = kPostRows;
   const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5, W = a.W, Wx = a.Wx;
@@ -719,6 +734,10 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
   uint32_t* cmask = reinterpret_cast<uint32_t*>(xr + (R + 1) * Wx); // [R+1][64]
   int* prevLast = reinterpret_cast<int*>(cmask + (R + 1) * 64);    // [R+1][64]
   int* nextFirst = prevLast + (R + 1) * 64;                        // [R+1][64]
+  uint16_t* sPix = reinterpret_cast<uint16_t*>(nextFirst + (R + 1) * 64);  // [R+1][Wsp]
+  uint8_t* sDL = reinterpret_cast<uint8_t*>(sPix + (R + 1) * Wsp);         // [R+3][Wsp]
+  uint8_t* sDR = sDL + (R + 3) * Wsp;                                      // [R+3][Wsp]
+  uint8_t* sLo = sDR + (R + 3) * Wsp;                                      // [R+1][Wx] L_org rows
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int y0 = blockIdx.x * R;
@@ -726,17 +745,31 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
   const int nf = a.K == 2 ? min(nr + 1, a.Hs - y0) : nr;     // fill rows needed (SU reads y+1)
   const float thr = (float)(a.K * a.T);
 
-  // 1. masked rows y0-1 .. y0+nf (clamped), Eq. 10
+  // 0. stage every input row in shared memory: one batch of independent loads
   for (int r = 0; r < nf + 2; ++r) {
-    const int yy = clampi(y0 - 1 + r, 0, a.Hs - 1);
-    const uint8_t* dl = a.DL + (size_t)yy * Ws;
-    const uint8_t* dr = a.DR + (size_t)yy * Ws;
+    const size_t o = (size_t)clampi(y0 - 1 + r, 0, a.Hs - 1) * Ws;
+#pragma unroll 4
     for (int x = tid; x < Ws; x += blockDim.x) {
-      const int k = __ldg(dl + x);
-      const bool gcp = (x - k >= 0) && (__ldg(dr + x - k) == k);
-      mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+      sDL[r * Wsp + x] = __ldg(a.DL + o + x);
+      sDR[r * Wsp + x] = __ldg(a.DR + o + x);
     }
   }
+  for (int j = 0; j < nf; ++j) {
+#pragma unroll 4
+    for (int x = tid; x < Ws; x += blockDim.x) sPix[j * Wsp + x] = __ldg(a.pixL + (size_t)(y0 + j) * Ws + x);
+    if (a.K == 2) {
+#pragma unroll 4
+      for (int X = tid; X < W; X += blockDim.x) sLo[j * Wx + X] = __ldg(a.Lorg + (size_t)(2 * (y0 + j)) * W + X);
+    }
+  }
+  __syncthreads();
+  // 1. masked rows y0-1 .. y0+nf (clamped), Eq. 10
+  for (int r = 0; r < nf + 2; ++r)
+    for (int x = tid; x < Ws; x += blockDim.x) {
+      const int k = sDL[r * Wsp + x];
+      const bool gcp = (x - k >= 0) && (sDR[r * Wsp + x - k] == k);
+      mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+    }
   __syncthreads();
   // 2. median rows y0 .. y0+nf-1
   for (int j = 0; j < nf; ++j) {
@@ -823,7 +856,7 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
   // 5. fill values of rows y0 .. y0+nf-1
   for (int j = 0; j < nf; ++j) {
     const uint8_t* mdr = md + j * Wsp;
-    const uint16_t* pix = a.pixL + (size_t)(y0 + j) * Ws;
+    const uint16_t* pix = sPix + j * Wsp;
     for (int x = tid; x < Ws; x += blockDim.x) {
       float v;
       if (mdr[x] != kInvalid) {
@@ -846,7 +879,7 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
     // 6a. x pass of Step8 on the seeded rows: xr[j][X] for X < W (pairs 2p, 2p+1)
     for (int j = 0; j < nf; ++j) {
       const float* f = fv + j * Wsp;
-      const uint8_t* L = a.Lorg + (size_t)(2 * (y0 + j)) * W;
+      const uint8_t* L = sLo + j * Wx;
       float* o = xr + j * Wx;
       for (int p = tid; 2 * p < W; p += blockDim.x) {
         if (p < Ws) {
@@ -859,8 +892,8 @@ __global__ void __launch_bounds__(256) post_kernel(PostArgs a) {
               if (fabsf(__fsub_rn(av, bv)) <= thr) {
                 v = __fmul_rn(__fadd_rn(av, bv), 0.5f);
               } else {
-                const int c = __ldg(L + 2 * p + 1);
-                v = (abs((int)__ldg(L + 2 * p) - c) <= abs((int)__ldg(L + 2 * p + 2) - c)) ? av : bv;
+                const int c = L[2 * p + 1];
+                v = (abs((int)L[2 * p] - c) <= abs((int)L[2 * p + 2] - c)) ? av : bv;
               }
             }
             o[2 * p + 1] = v;
@@ -962,7 +995,7 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.Wsp = (g.Ws + 31) & ~31;
   a.Wx = (g.W + 3) & ~3;
-  post_kernel<<<(g.Hs + kPostRows - 1) / kPostRows, 256, p.post_smem, s>>>(a);
+  post_kernel<<<(g.Hs + kPostRows - 1) / kPostRows, 512, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1009,7 +1042,8 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   const int Wsp = (g.Ws + 31) & ~31;
   const int Wx = (g.W + 3) & ~3;
   p.post_smem = (kPostRows + 3) * Wsp + (kPostRows + 1) * Wsp + (kPostRows + 1) * Wsp * 4 +
-                (kPostRows + 1) * Wx * 4 + 3 * (kPostRows + 1) * 64 * 4 + 64;
+                (kPostRows + 1) * Wx * 4 + 3 * (kPostRows + 1) * 64 * 4 +
+                (kPostRows + 1) * Wsp * 2 + 2 * (kPostRows + 3) * Wsp + (kPostRows + 1) * Wx + 64;
   if (p.post_smem > 48 * 1024 &&
       (e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
     return e;
