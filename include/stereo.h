@@ -92,7 +92,8 @@ void stereo_default_params(stereo_params* p);
  * t_fill >= 0, w_x >= 0, w_y >= 0, k_scale >= 1, D >= 1, W >= 1, H >= 1,
  * W/K >= 1, H/K >= 1, six distinct non-zero census offsets -> STEREO_EINVAL.
  * STEREO_EUNSUPPORTED for K not in {1,2}, ceil(D/K) > 255 (u8 maps use 255 as
- * INVALID), w_x or w_y > 254 (u8 arms), census offsets beyond +-2, m_pool > 3.
+ * INVALID), w_x > 254 (u8 arms), w_y > 112 (the y-aggregation tile holds
+ * B + 2*w_y <= 240 rows), census offsets beyond +-2, m_pool > 3.
  * Allocates every device buffer (dominant: two u32 CA_x volumes of
  * Ds*Hs*Ws*4 bytes each), builds the fixed-point cost tables on the host in
  * double precision and uploads them.  No kernel runs.  On success *out owns

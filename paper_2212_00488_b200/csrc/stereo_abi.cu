@@ -267,9 +267,9 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
     delete h;
     return fail(STEREO_EUNSUPPORTED, "scaled width %d exceeds 2016", g.Ws);
   }
-  if (g.w_y > 124) {
+  if (g.w_y > 112) {
     delete h;
-    return fail(STEREO_EUNSUPPORTED, "w_y > 124 not supported by the y-aggregation tile");
+    return fail(STEREO_EUNSUPPORTED, "w_y > 112 not supported by the y-aggregation tile");
   }
   cudaError_t e = cudaGetDevice(&h->device);
   if (e != cudaSuccess) {

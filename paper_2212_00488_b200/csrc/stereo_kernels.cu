@@ -419,16 +419,19 @@ cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t 
 
 // ============================================================================
 // YPASS — y aggregation (Eq. 8) + WTA (Eq. 9) for one
-// base, Step5.  CTA = 32-column strip x B output rows, looping over
-// d.  Per d a TMA 3-D box {32 columns, T = 8*SEG rows, 1 disparity} of the
+// base, Step5.  CTA = 16-column strip x B output rows, looping over
+// d.  Per d a TMA 3-D box {16 columns, TB = 16*SEG rows, 1 disparity} of the
 // CA_x volume starting at row y0 - w_y lands in shared memory (rows outside
 // the image are zero-filled by the TMA unit: they never enter a window);
 // two stages, mbarrier-completed, refilled as soon as a stage is consumed.
-// Each warp scans SEG rows of the tile serially in registers (u64, exact),
-// segment offsets go through shared memory, the exact column prefix E lands in
-// shared memory, and every output pixel takes CA = E[y+N+1] - E[y-M] (O(1)
+// Thread (col = t & 15, seg = t >> 4) scans SEG rows of its column serially in
+// registers (u64, exact); the two segments of a warp combine by shuffle, the
+// eight warp totals through shared memory; the exact column prefix E lands in
+// shared memory and every output pixel takes CA = E[y+N+1] - E[y-M] (O(1)
 // instead of O(W_y)) and keeps the running minimum with the paper's strict
-// "<": ties keep the smallest d.
+// "<": ties keep the smallest d.  SEG is odd so the two half-warps'
+// tile rows fall in disjoint banks; 16-column strips allow tall tiles (small
+// halo ratio TB/B) at good grid balance.
 // ============================================================================
 struct YArgs {
   const uint32_t* arm0;
@@ -440,8 +443,9 @@ struct YArgs {
   int Ws, Hs, Ds, w_y, B;
 };
 
-constexpr int kYWarps = 8;
-constexpr int kYRPT = 12;  // output rows per thread (B <= 96)
+constexpr int kYThreads = 256;
+constexpr int kYSegs = 16;   // row segments per CTA (2 per warp)
+constexpr int kYRPT = 12;    // output rows per thread (B <= 192)
 constexpr int kYStages = 2;
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -472,38 +476,40 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 }
 
 template <int SEG>
-__global__ void __launch_bounds__(kYWarps * 32, 2)
+__global__ void __launch_bounds__(kYThreads, 2)
     ypass_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
                  YArgs a) {
-  constexpr int TB = kYWarps * SEG;  // tile rows = TMA box height
-  constexpr uint32_t kTileBytes = TB * 32 * 4;
+  static_assert(SEG & 1, "SEG must be odd (bank-disjoint half-warps)");
+  constexpr int TB = kYSegs * SEG;  // tile rows = TMA box height
+  constexpr uint32_t kTileBytes = TB * 16 * 4;
   extern __shared__ __align__(128) uint8_t ysm[];  // TMA destinations need 128-B alignment
-  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                      // [kYStages][TB][32]
-  uint64_t* E = reinterpret_cast<uint64_t*>(ysm + kYStages * kTileBytes);  // [TB+1][32]
-  uint64_t* tot = E + (TB + 1) * 32;                                       // [kYWarps][32]
-  uint64_t* bar = tot + kYWarps * 32;                                      // [kYStages]
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                       // [kYStages][TB][16]
+  uint64_t* E = reinterpret_cast<uint64_t*>(ysm + kYStages * kTileBytes);  // [TB+1][16]
+  uint64_t* tot = E + (TB + 1) * 16;                                       // [8][16]
+  uint64_t* bar = tot + 8 * 16;                                            // [kYStages]
+  const int tid = threadIdx.x, w = tid >> 5;
+  const int col = tid & 15, seg = tid >> 4, upper = (tid >> 4) & 1;
   const int base = blockIdx.z;
   const CUtensorMap* tm = base ? &tm1 : &tm0;
   const uint32_t* armp = base ? a.arm1 : a.arm0;
   uint8_t* dmap = base ? a.D1 : a.D0;
   uint64_t* cadbg = base ? a.ca1 : a.ca0;
-  const int x0 = blockIdx.x * 32, x = x0 + lane;
+  const int x0 = blockIdx.x * 16, x = x0 + col;
   const int y0 = blockIdx.y * a.B, yt0 = y0 - a.w_y;
   const int Ds = a.Ds;
 
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     for (int s = 0; s < kYStages && s < Ds; ++s) {
       mbar_expect_tx(bar + s, kTileBytes);
-      tma_load_3d(tile + s * TB * 32, tm, bar + s, x0, yt0, s);
+      tma_load_3d(tile + s * TB * 16, tm, bar + s, x0, yt0, s);
     }
   }
-  if (w == 0) E[lane] = 0;
+  if (tid < 16) E[tid] = 0;
 
   // window byte offsets into E (d-invariant) and running minima
   uint32_t oa[kYRPT], ob[kYRPT];
@@ -511,44 +517,46 @@ __global__ void __launch_bounds__(kYWarps * 32, 2)
   int bd[kYRPT];
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
-    const int yl = w * kYRPT + r, y = y0 + yl;
-    oa[r] = lane * 8u;
-    ob[r] = lane * 8u;
+    const int yl = seg * kYRPT + r, y = y0 + yl;
+    oa[r] = col * 8u;
+    ob[r] = col * 8u;
     best[r] = ~0ull;
     bd[r] = 0;
     if (yl < a.B && y < a.Hs && x < a.Ws) {
       const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
       const int M = (arm >> 16) & 255u, N = arm >> 24;
-      oa[r] = ((uint32_t)(y - M - yt0) * 32u + lane) * 8u;
-      ob[r] = ((uint32_t)(y + N + 1 - yt0) * 32u + lane) * 8u;
+      oa[r] = ((uint32_t)(y - M - yt0) * 16u + col) * 8u;
+      ob[r] = ((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u;
     }
   }
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
-  uint64_t* Ew = E + (w * SEG + 1) * 32 + lane;
+  uint64_t* Ew = E + (seg * SEG + 1) * 16 + col;
 
 #pragma unroll 1
   for (int d = 0; d < Ds; ++d) {
     const int st = d & 1;
     mbar_wait(bar + st, (d >> 1) & 1);
-    const uint32_t* tl = tile + st * TB * 32 + w * SEG * 32 + lane;
+    const uint32_t* tl = tile + st * TB * 16 + seg * SEG * 16 + col;
     uint64_t loc[SEG];
     uint64_t acc = 0;
 #pragma unroll
     for (int s = 0; s < SEG; ++s) {
-      acc += tl[s * 32];
+      acc += tl[s * 16];
       loc[s] = acc;
     }
-    tot[w * 32 + lane] = acc;
-    __syncthreads();  // (1) tile[st] consumed, segment totals visible
-    if (threadIdx.x == 0 && d + kYStages < Ds) {
+    // the warp's two segments: the upper half adds the lower half's total
+    const uint64_t low = __shfl_sync(kFull, acc, col);
+    if (upper) tot[w * 16 + col] = low + acc;
+    __syncthreads();  // (1) tile[st] consumed, warp totals visible
+    if (tid == 0 && d + kYStages < Ds) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar + st, kTileBytes);
-      tma_load_3d(tile + st * TB * 32, tm, bar + st, x0, yt0, d + kYStages);
+      tma_load_3d(tile + st * TB * 16, tm, bar + st, x0, yt0, d + kYStages);
     }
-    uint64_t off = 0;
-    for (int q = 0; q < w; ++q) off += tot[q * 32 + lane];
+    uint64_t off = upper ? low : 0ull;
+    for (int q = 0; q < w; ++q) off += tot[q * 16 + col];
 #pragma unroll
-    for (int s = 0; s < SEG; ++s) Ew[s * 32] = loc[s] + off;
+    for (int s = 0; s < SEG; ++s) Ew[s * 16] = loc[s] + off;
     __syncthreads();  // (2) column prefix complete
 #pragma unroll
     for (int r = 0; r < kYRPT; ++r) {
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 2)
     if (cadbg) {
 #pragma unroll
       for (int r = 0; r < kYRPT; ++r) {
-        const int yl = w * kYRPT + r, y = y0 + yl;
+        const int yl = seg * kYRPT + r, y = y0 + yl;
         if (yl < a.B && y < a.Hs && x < a.Ws)
           cadbg[((size_t)d * a.Hs + y) * a.Ws + x] =
               *reinterpret_cast<const uint64_t*>(Eb + ob[r]) -
@@ -569,33 +577,32 @@ __global__ void __launch_bounds__(kYWarps * 32, 2)
   }
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
-    const int yl = w * kYRPT + r, y = y0 + yl;
+    const int yl = seg * kYRPT + r, y = y0 + yl;
     if (yl < a.B && y < a.Hs && x < a.Ws) dmap[(size_t)y * a.Ws + x] = (uint8_t)bd[r];
   }
 }
 
 #define YPASS_DISPATCH(S_, EXPR)                       \
   switch (S_) {                                        \
-    case 8: { constexpr int SS = 8; EXPR; } break;     \
-    case 12: { constexpr int SS = 12; EXPR; } break;   \
-    case 16: { constexpr int SS = 16; EXPR; } break;   \
-    case 20: { constexpr int SS = 20; EXPR; } break;   \
-    case 24: { constexpr int SS = 24; EXPR; } break;   \
-    case 28: { constexpr int SS = 28; EXPR; } break;   \
-    case 32: { constexpr int SS = 32; EXPR; } break;   \
+    case 5: { constexpr int SS = 5; EXPR; } break;     \
+    case 7: { constexpr int SS = 7; EXPR; } break;     \
+    case 9: { constexpr int SS = 9; EXPR; } break;     \
+    case 11: { constexpr int SS = 11; EXPR; } break;   \
+    case 13: { constexpr int SS = 13; EXPR; } break;   \
+    case 15: { constexpr int SS = 15; EXPR; } break;   \
     default: break;                                    \
   }
 
 static int ypass_seg_for(int T) {
-  const int need = (T + kYWarps - 1) / kYWarps;
-  for (int s : {8, 12, 16, 20, 24, 28, 32})
+  const int need = (T + kYSegs - 1) / kYSegs;
+  for (int s : {5, 7, 9, 11, 13, 15})
     if (s >= need) return s;
   return 0;
 }
 
 static int ypass_smem_bytes(int SEG) {
-  const int TB = kYWarps * SEG;
-  return kYStages * TB * 32 * 4 + (TB + 1) * 32 * 8 + kYWarps * 32 * 8 + kYStages * 8;
+  const int TB = kYSegs * SEG;
+  return kYStages * TB * 16 * 4 + (TB + 1) * 16 * 8 + 8 * 16 * 8 + kYStages * 8;
 }
 
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
@@ -606,10 +613,10 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
-  dim3 grid((g.Ws + 31) / 32, p.ypass_nb, 2);
+  dim3 grid((g.Ws + 15) / 16, p.ypass_nb, 2);
   cudaError_t e = cudaErrorInvalidValue;
   YPASS_DISPATCH(p.ypass_SEG,
-                 (ypass_kernel<SS><<<grid, kYWarps * 32, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
+                 (ypass_kernel<SS><<<grid, kYThreads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
                   e = cudaGetLastError()));
   return e;
 }
@@ -1019,7 +1026,7 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
   }
   cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)g.Ds};
   cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 4, (cuuint64_t)g.Wp * g.Hs * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1069,8 +1076,9 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   const int units = g.Hs * ((g.Ds + kXDPerUnit - 1) / kXDPerUnit);
   p.xpass_grid = units < occ * nsm ? units : occ * nsm;
   // YPASS: choose the number of tiles per strip balancing halo cost and waves
-  const int strips = (g.Ws + 31) / 32;
-  const int nb0 = (g.Hs + kYWarps * kYRPT - 1) / (kYWarps * kYRPT);
+  // (per-CTA shared wavefronts per d ~ 1.5*TB + 2*B + tot exchange)
+  const int strips = (g.Ws + 15) / 16;
+  const int nb0 = (g.Hs + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
   p.ypass_nb = 0;
   for (int nb = nb0; nb <= g.Hs && nb <= 4 * nb0 + 8; ++nb) {
@@ -1078,11 +1086,10 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     const int SEG = ypass_seg_for(B + 2 * g.w_y);
     if (!SEG) continue;
     const int smem = ypass_smem_bytes(SEG);
-    if (smem > 227 * 1024) continue;
     const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
     const int ctas = strips * nb * 2;
     const double waves = (double)((ctas + nsm * per_sm - 1) / (nsm * per_sm));
-    const double cost = waves * per_sm * (6.0 * kYWarps * SEG + 10.0 * B);
+    const double cost = waves * per_sm * (1.5 * kYSegs * SEG + 2.0 * B + 56.0);
     if (cost < best - 1e-9) {
       best = cost;
       p.ypass_nb = nb; p.ypass_B = B; p.ypass_SEG = SEG; p.ypass_smem = smem;
@@ -1093,8 +1100,8 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        p.ypass_smem));
   if (e != cudaSuccess) return e;
-  if ((e = make_tmap(&p.tmL, b.caxL, g, kYWarps * p.ypass_SEG))) return e;
-  if ((e = make_tmap(&p.tmR, b.caxR, g, kYWarps * p.ypass_SEG))) return e;
+  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG))) return e;
+  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG))) return e;
   return cudaSuccess;
 }
 
