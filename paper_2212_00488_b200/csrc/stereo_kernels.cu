@@ -440,7 +440,7 @@ struct YArgs {
   uint8_t* D1;
   uint64_t* ca0;  // debug (may be null)
   uint64_t* ca1;
-  int Ws, Hs, Ds, w_y, B;
+  int Ws, Hs, Ds, w_y, B, kb;
 };
 
 constexpr int kYThreads = 256;
@@ -475,18 +475,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-template <int SEG>
+// Two disparities per iteration in split precision.  Every CA_x value is
+// < 2^32 (choice of f, R12c); split it as x = hi*2^kb + lo with lo < 2^kb,
+// kb = 32 - ceil(log2(2 w_y + 1)): over any window of <= 2 w_y + 1 rows the lo
+// sum is < 2^32 and the hi sum < 2^16, so the column prefixes can be kept
+// modulo 2^32 (lo of d and d+1) and modulo 2^16 (hi of d in the low half, of
+// d+1 in the high half of one u32) and every window difference is still exact:
+// CA = (lo_b - lo_a) + ((hi_b - hi_a) << kb).  12 bytes of prefix per two
+// disparities instead of 16, i.e. fewer shared-memory wavefronts per output.
+template <int SEG, bool DBG>
 __global__ void __launch_bounds__(kYThreads, 2)
     ypass_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
                  YArgs a) {
   static_assert(SEG & 1, "SEG must be odd (bank-disjoint half-warps)");
-  constexpr int TB = kYSegs * SEG;  // tile rows = TMA box height
-  constexpr uint32_t kTileBytes = TB * 16 * 4;
+  constexpr int TB = kYSegs * SEG;                 // tile rows = TMA box height
+  constexpr uint32_t kTileBytes = 2 * TB * 16 * 4;  // box {16, TB, 2}
   extern __shared__ __align__(128) uint8_t ysm[];  // TMA destinations need 128-B alignment
-  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                       // [kYStages][TB][16]
-  uint64_t* E = reinterpret_cast<uint64_t*>(ysm + kYStages * kTileBytes);  // [TB+1][16]
-  uint64_t* tot = E + (TB + 1) * 16;                                       // [8][16]
-  uint64_t* bar = tot + 8 * 16;                                            // [kYStages]
+  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                      // [kYStages][2][TB][16]
+  uint2* Elo = reinterpret_cast<uint2*>(ysm + kYStages * kTileBytes);      // [TB+1][16]
+  uint32_t* Ehi = reinterpret_cast<uint32_t*>(Elo + (TB + 1) * 16);       // [TB+1][16]
+  uint4* tot = reinterpret_cast<uint4*>(Ehi + (TB + 1) * 16);             // [8][16]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tot + 8 * 16);              // [kYStages]
   const int tid = threadIdx.x, w = tid >> 5;
   const int col = tid & 15, seg = tid >> 4, upper = (tid >> 4) & 1;
   const int base = blockIdx.z;
@@ -496,7 +505,8 @@ __global__ void __launch_bounds__(kYThreads, 2)
   uint64_t* cadbg = base ? a.ca1 : a.ca0;
   const int x0 = blockIdx.x * 16, x = x0 + col;
   const int y0 = blockIdx.y * a.B, yt0 = y0 - a.w_y;
-  const int Ds = a.Ds;
+  const int Ds = a.Ds, kb = a.kb;
+  const uint32_t lomask = (1u << kb) - 1u;
 
   if (tid == 0) {
     for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
@@ -504,81 +514,105 @@ __global__ void __launch_bounds__(kYThreads, 2)
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < kYStages && s < Ds; ++s) {
+    for (int s = 0; s < kYStages && 2 * s < Ds; ++s) {
       mbar_expect_tx(bar + s, kTileBytes);
-      tma_load_3d(tile + s * TB * 16, tm, bar + s, x0, yt0, s);
+      tma_load_3d(tile + s * 2 * TB * 16, tm, bar + s, x0, yt0, 2 * s);
     }
   }
-  if (tid < 16) E[tid] = 0;
+  if (tid < 16) {
+    Elo[tid] = make_uint2(0u, 0u);
+    Ehi[tid] = 0u;
+  }
 
-  // window byte offsets into E (d-invariant) and running minima
-  uint32_t oa[kYRPT], ob[kYRPT];
+  // window byte offsets into Elo (Ehi: half of it), packed a | b << 16
+  // (< 2^16: (TB+1)*16*8 <= 30848), and the running minima as keys
+  // CA << 8 | d (CA < 2^40, d < 256): the u64 minimum of the keys is the
+  // paper's strict-< scan, ties to the smallest d
+  uint32_t oab[kYRPT];
   uint64_t best[kYRPT];
-  int bd[kYRPT];
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
     const int yl = seg * kYRPT + r, y = y0 + yl;
-    oa[r] = col * 8u;
-    ob[r] = col * 8u;
+    oab[r] = (col * 8u) | ((col * 8u) << 16);
     best[r] = ~0ull;
-    bd[r] = 0;
     if (yl < a.B && y < a.Hs && x < a.Ws) {
       const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
       const int M = (arm >> 16) & 255u, N = arm >> 24;
-      oa[r] = ((uint32_t)(y - M - yt0) * 16u + col) * 8u;
-      ob[r] = ((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u;
+      oab[r] = (((uint32_t)(y - M - yt0) * 16u + col) * 8u) |
+               ((((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u) << 16);
     }
   }
-  const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
-  uint64_t* Ew = E + (seg * SEG + 1) * 16 + col;
+  const uint8_t* EloB = reinterpret_cast<const uint8_t*>(Elo);
+  const uint8_t* EhiB = reinterpret_cast<const uint8_t*>(Ehi);
+  uint2* Ew = Elo + (seg * SEG + 1) * 16 + col;
+  uint32_t* Hw = Ehi + (seg * SEG + 1) * 16 + col;
 
 #pragma unroll 1
-  for (int d = 0; d < Ds; ++d) {
-    const int st = d & 1;
-    mbar_wait(bar + st, (d >> 1) & 1);
-    const uint32_t* tl = tile + st * TB * 16 + seg * SEG * 16 + col;
-    uint64_t loc[SEG];
-    uint64_t acc = 0;
+  for (int d = 0; d < Ds; d += 2) {
+    const int it = d >> 1, st = it & 1;
+    mbar_wait(bar + st, (it >> 1) & 1);
+    const uint32_t* t0 = tile + st * 2 * TB * 16 + seg * SEG * 16 + col;
+    const uint32_t* t1 = t0 + TB * 16;
+    uint32_t l0[SEG], l1[SEG], lh[SEG];
+    uint32_t a0 = 0, a1 = 0, ah = 0;
 #pragma unroll
     for (int s = 0; s < SEG; ++s) {
-      acc += tl[s * 16];
-      loc[s] = acc;
+      const uint32_t v0 = t0[s * 16], v1 = t1[s * 16];
+      a0 += v0 & lomask;
+      a1 += v1 & lomask;
+      ah += (v0 >> kb) | ((v1 >> kb) << 16);
+      l0[s] = a0; l1[s] = a1; lh[s] = ah;
     }
-    // the warp's two segments: the upper half adds the lower half's total
-    const uint64_t low = __shfl_sync(kFull, acc, col);
-    if (upper) tot[w * 16 + col] = low + acc;
+    // the warp's two segments: the upper half adds the lower half's totals
+    const uint32_t b0 = __shfl_sync(kFull, a0, col), b1 = __shfl_sync(kFull, a1, col),
+                   bh = __shfl_sync(kFull, ah, col);
+    if (upper) tot[w * 16 + col] = make_uint4(b0 + a0, b1 + a1, bh + ah, 0u);
     __syncthreads();  // (1) tile[st] consumed, warp totals visible
-    if (tid == 0 && d + kYStages < Ds) {
+    if (tid == 0 && d + 2 * kYStages < Ds) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar + st, kTileBytes);
-      tma_load_3d(tile + st * TB * 16, tm, bar + st, x0, yt0, d + kYStages);
+      tma_load_3d(tile + st * 2 * TB * 16, tm, bar + st, x0, yt0, d + 2 * kYStages);
     }
-    uint64_t off = upper ? low : 0ull;
-    for (int q = 0; q < w; ++q) off += tot[q * 16 + col];
+    uint32_t o0 = upper ? b0 : 0u, o1 = upper ? b1 : 0u, oh = upper ? bh : 0u;
+    for (int q = 0; q < w; ++q) {
+      const uint4 t = tot[q * 16 + col];
+      o0 += t.x; o1 += t.y; oh += t.z;
+    }
 #pragma unroll
-    for (int s = 0; s < SEG; ++s) Ew[s * 16] = loc[s] + off;
-    __syncthreads();  // (2) column prefix complete
+    for (int s = 0; s < SEG; ++s) {
+      Ew[s * 16] = make_uint2(l0[s] + o0, l1[s] + o1);
+      Hw[s * 16] = lh[s] + oh;
+    }
+    __syncthreads();  // (2) column prefixes complete
+    const bool two = d + 1 < Ds;
 #pragma unroll
     for (int r = 0; r < kYRPT; ++r) {
-      const uint64_t ca = *reinterpret_cast<const uint64_t*>(Eb + ob[r]) -
-                          *reinterpret_cast<const uint64_t*>(Eb + oa[r]);
-      if (ca < best[r]) { best[r] = ca; bd[r] = d; }
-    }
-    if (cadbg) {
-#pragma unroll
-      for (int r = 0; r < kYRPT; ++r) {
+      // opaque to the optimiser: keeps it from hoisting 4 d-invariant
+      // addresses per output out of the d loop (register spills)
+      uint32_t v = oab[r];
+      asm volatile("" : "+r"(v));
+      const uint32_t ia = v & 0xffffu, ib = v >> 16;
+      const uint2 la = *reinterpret_cast<const uint2*>(EloB + ia);
+      const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
+      const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
+                          *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
+      const uint64_t c0 = (uint64_t)(lb.x - la.x) + ((uint64_t)(dh & 0xffffu) << kb);
+      const uint64_t c1 = (uint64_t)(lb.y - la.y) + ((uint64_t)(dh >> 16) << kb);
+      best[r] = min(best[r], (c0 << 8) | (uint32_t)d);
+      if (two) best[r] = min(best[r], (c1 << 8) | (uint32_t)(d + 1));
+      if (DBG) {
         const int yl = seg * kYRPT + r, y = y0 + yl;
-        if (yl < a.B && y < a.Hs && x < a.Ws)
-          cadbg[((size_t)d * a.Hs + y) * a.Ws + x] =
-              *reinterpret_cast<const uint64_t*>(Eb + ob[r]) -
-              *reinterpret_cast<const uint64_t*>(Eb + oa[r]);
+        if (yl < a.B && y < a.Hs && x < a.Ws) {
+          cadbg[((size_t)d * a.Hs + y) * a.Ws + x] = c0;
+          if (two) cadbg[((size_t)(d + 1) * a.Hs + y) * a.Ws + x] = c1;
+        }
       }
     }
   }
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
     const int yl = seg * kYRPT + r, y = y0 + yl;
-    if (yl < a.B && y < a.Hs && x < a.Ws) dmap[(size_t)y * a.Ws + x] = (uint8_t)bd[r];
+    if (yl < a.B && y < a.Hs && x < a.Ws) dmap[(size_t)y * a.Ws + x] = (uint8_t)(best[r] & 255u);
   }
 }
 
@@ -602,7 +636,14 @@ static int ypass_seg_for(int T) {
 
 static int ypass_smem_bytes(int SEG) {
   const int TB = kYSegs * SEG;
-  return kYStages * TB * 16 * 4 + (TB + 1) * 16 * 8 + 8 * 16 * 8 + kYStages * 8;
+  return kYStages * 2 * TB * 16 * 4 + (TB + 1) * 16 * 12 + 8 * 16 * 16 + kYStages * 8;
+}
+
+// split bit of the two-disparity prefix: (2 w_y + 1) * 2^kb <= 2^32
+static int ypass_split_bits(int w_y) {
+  int lg = 0;
+  while ((1 << lg) < 2 * w_y + 1) ++lg;
+  return lg == 0 ? 31 : 32 - lg;
 }
 
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
@@ -613,11 +654,17 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
+  a.kb = ypass_split_bits(g.w_y);
   dim3 grid((g.Ws + 15) / 16, p.ypass_nb, 2);
   cudaError_t e = cudaErrorInvalidValue;
-  YPASS_DISPATCH(p.ypass_SEG,
-                 (ypass_kernel<SS><<<grid, kYThreads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
-                  e = cudaGetLastError()));
+  if (store_ca)
+    YPASS_DISPATCH(p.ypass_SEG,
+                   (ypass_kernel<SS, true><<<grid, kYThreads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
+                    e = cudaGetLastError()))
+  else
+    YPASS_DISPATCH(p.ypass_SEG,
+                   (ypass_kernel<SS, false><<<grid, kYThreads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
+                    e = cudaGetLastError()))
   return e;
 }
 
@@ -1014,7 +1061,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows) {
+static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows,
+                             int box_d) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1026,7 +1074,7 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
   }
   cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)g.Ds};
   cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 4, (cuuint64_t)g.Wp * g.Hs * 4};
-  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, (cuuint32_t)box_d};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1076,7 +1124,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   const int units = g.Hs * ((g.Ds + kXDPerUnit - 1) / kXDPerUnit);
   p.xpass_grid = units < occ * nsm ? units : occ * nsm;
   // YPASS: choose the number of tiles per strip balancing halo cost and waves
-  // (per-CTA shared wavefronts per d ~ 1.5*TB + 2*B + tot exchange)
+  // (per-CTA shared wavefronts per d ~ 1.25*TB + 1.75*B + tot exchange)
   const int strips = (g.Ws + 15) / 16;
   const int nb0 = (g.Hs + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
@@ -1089,19 +1137,23 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
     const int ctas = strips * nb * 2;
     const double waves = (double)((ctas + nsm * per_sm - 1) / (nsm * per_sm));
-    const double cost = waves * per_sm * (1.5 * kYSegs * SEG + 2.0 * B + 56.0);
+    const double cost = waves * per_sm * (1.25 * kYSegs * SEG + 1.75 * B + 20.0);
     if (cost < best - 1e-9) {
       best = cost;
       p.ypass_nb = nb; p.ypass_B = B; p.ypass_SEG = SEG; p.ypass_smem = smem;
     }
   }
   if (!p.ypass_nb) return cudaErrorInvalidValue;
-  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS>,
+  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS, false>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        p.ypass_smem));
   if (e != cudaSuccess) return e;
-  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG))) return e;
-  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG))) return e;
+  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS, true>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       p.ypass_smem));
+  if (e != cudaSuccess) return e;
+  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG, 2))) return e;
+  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG, 2))) return e;
   return cudaSuccess;
 }
 
