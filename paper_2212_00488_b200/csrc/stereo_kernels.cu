@@ -440,7 +440,7 @@ struct YArgs {
   uint8_t* D1;
   uint64_t* ca0;  // debug (may be null)
   uint64_t* ca1;
-  int Ws, Hs, Ds, w_y, B, kb;
+  int Ws, Hs, Ds, w_y, B;
 };
 
 constexpr int kYThreads = 256;
@@ -476,13 +476,57 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 }
 
 // Two disparities per iteration in split precision.  Every CA_x value is
-// < 2^32 (choice of f, R12c); split it as x = hi*2^kb + lo with lo < 2^kb,
-// kb = 32 - ceil(log2(2 w_y + 1)): over any window of <= 2 w_y + 1 rows the lo
-// sum is < 2^32 and the hi sum < 2^16, so the column prefixes can be kept
-// modulo 2^32 (lo of d and d+1) and modulo 2^16 (hi of d in the low half, of
-// d+1 in the high half of one u32) and every window difference is still exact:
-// CA = (lo_b - lo_a) + ((hi_b - hi_a) << kb).  12 bytes of prefix per two
+// < 2^32 (choice of f, R12c); split it as x = hi*2^24 + lo with lo < 2^24:
+// over any window of <= 2 w_y + 1 <= 225 rows the lo sum is < 2^32 and the hi
+// sum < 2^16, so the column prefixes can be kept modulo 2^32 (lo of d and
+// d+1) and modulo 2^16 (hi of d in the low half, of d+1 in the high half of one
+// u32) and every window difference is still exact:
+// CA = (lo_b - lo_a) + ((hi_b - hi_a) << 24).  12 bytes of prefix per two
 // disparities instead of 16, i.e. fewer shared-memory wavefronts per output.
+// The argmin key CA << 8 | d (CA < 2^40, d < 256) is then two 32-bit words
+// {lo << 8 | d, (lo >> 24) + hi}: two ALU operations, no 64-bit shifts; the u64
+// minimum of the keys is the paper's strict-< scan with ties to the smallest
+// d.
+constexpr int kYSplit = 24;
+
+template <bool DBG>
+__device__ __forceinline__ void ypass_take(uint64_t& best, uint32_t lo, uint32_t hi, int d,
+                                           uint64_t* cadbg, size_t dbg_idx) {
+  const uint32_t klo = (lo << 8) | (uint32_t)d;
+  const uint32_t khi = (lo >> 24) + hi;
+  const uint64_t key = ((uint64_t)khi << 32) | klo;
+  best = min(best, key);
+  if (DBG && cadbg) cadbg[dbg_idx] = key >> 8;
+}
+
+// WTA over the window sums of d (and d+1 if TWO) for the thread's outputs.
+template <bool TWO, bool DBG>
+__device__ __forceinline__ void ypass_wta(uint64_t (&best)[kYRPT], const uint32_t (&oab)[kYRPT],
+                                          int nr, uint32_t elo, uint32_t ehi, int d,
+                                          uint64_t* cadbg, const YArgs& a, int yrow0, int x) {
+#pragma unroll
+  for (int r = 0; r < kYRPT; ++r) {
+    if (r < nr) {
+      // opaque to the optimiser: keeps it from hoisting 4 d-invariant
+      // addresses per output out of the d loop (register spills)
+      uint32_t v = oab[r];
+      asm volatile("" : "+r"(v));
+      const uint32_t ia = v & 0xffffu, ib = v >> 16;
+      uint32_t la0, la1, lb0, lb1, ha, hb;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(la0), "=r"(la1) : "r"(elo + ia));
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lb0), "=r"(lb1) : "r"(elo + ib));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ha) : "r"(ehi + (ia >> 1)));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hb) : "r"(ehi + (ib >> 1)));
+      const uint32_t dh = hb - ha;
+      const size_t di = DBG ? ((size_t)d * a.Hs + yrow0 + 16 * r) * a.Ws + x : 0;
+      ypass_take<DBG>(best[r], lb0 - la0, dh & 0xffffu, d, cadbg, di);
+      if (TWO)
+        ypass_take<DBG>(best[r], lb1 - la1, dh >> 16, d + 1, cadbg,
+                        di + (DBG ? (size_t)a.Hs * a.Ws : 0));
+    }
+  }
+}
+
 template <int SEG, bool DBG>
 __global__ void __launch_bounds__(kYThreads, 2)
     ypass_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
@@ -505,8 +549,11 @@ __global__ void __launch_bounds__(kYThreads, 2)
   uint64_t* cadbg = base ? a.ca1 : a.ca0;
   const int x0 = blockIdx.x * 16, x = x0 + col;
   const int y0 = blockIdx.y * a.B, yt0 = y0 - a.w_y;
-  const int Ds = a.Ds, kb = a.kb;
-  const uint32_t lomask = (1u << kb) - 1u;
+  const int Ds = a.Ds;
+  // output rows of this thread: y0 + seg + 16 r, r < nr (interleaved, so the
+  // rows past B are whole trailing iterations, mostly warp-uniform)
+  const int nrow = min(a.B, a.Hs - y0);
+  const int nr = x < a.Ws ? max(0, (nrow - seg + 15) >> 4) : 0;
 
   if (tid == 0) {
     for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
@@ -525,27 +572,25 @@ __global__ void __launch_bounds__(kYThreads, 2)
   }
 
   // window byte offsets into Elo (Ehi: half of it), packed a | b << 16
-  // (< 2^16: (TB+1)*16*8 <= 30848), and the running minima as keys
-  // CA << 8 | d (CA < 2^40, d < 256): the u64 minimum of the keys is the
-  // paper's strict-< scan, ties to the smallest d
+  // (< 2^16: (TB+1)*16*8 <= 30848), and the running minimum keys
   uint32_t oab[kYRPT];
   uint64_t best[kYRPT];
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
-    const int yl = seg * kYRPT + r, y = y0 + yl;
-    oab[r] = (col * 8u) | ((col * 8u) << 16);
+    const int y = y0 + seg + 16 * r;
+    oab[r] = 0u;
     best[r] = ~0ull;
-    if (yl < a.B && y < a.Hs && x < a.Ws) {
+    if (r < nr) {
       const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
       const int M = (arm >> 16) & 255u, N = arm >> 24;
       oab[r] = (((uint32_t)(y - M - yt0) * 16u + col) * 8u) |
                ((((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u) << 16);
     }
   }
-  const uint8_t* EloB = reinterpret_cast<const uint8_t*>(Elo);
-  const uint8_t* EhiB = reinterpret_cast<const uint8_t*>(Ehi);
+  const uint32_t ysm_elo = smem_u32(Elo), ysm_ehi = smem_u32(Ehi);
   uint2* Ew = Elo + (seg * SEG + 1) * 16 + col;
   uint32_t* Hw = Ehi + (seg * SEG + 1) * 16 + col;
+  constexpr uint32_t kLoMask = (1u << kYSplit) - 1u;
 
 #pragma unroll 1
   for (int d = 0; d < Ds; d += 2) {
@@ -558,9 +603,9 @@ __global__ void __launch_bounds__(kYThreads, 2)
 #pragma unroll
     for (int s = 0; s < SEG; ++s) {
       const uint32_t v0 = t0[s * 16], v1 = t1[s * 16];
-      a0 += v0 & lomask;
-      a1 += v1 & lomask;
-      ah += (v0 >> kb) | ((v1 >> kb) << 16);
+      a0 += v0 & kLoMask;
+      a1 += v1 & kLoMask;
+      ah += (v0 >> kYSplit) | ((v1 >> (kYSplit - 16)) & 0xffff0000u);
       l0[s] = a0; l1[s] = a1; lh[s] = ah;
     }
     // the warp's two segments: the upper half adds the lower half's totals
@@ -584,36 +629,14 @@ __global__ void __launch_bounds__(kYThreads, 2)
       Hw[s * 16] = lh[s] + oh;
     }
     __syncthreads();  // (2) column prefixes complete
-    const bool two = d + 1 < Ds;
-#pragma unroll
-    for (int r = 0; r < kYRPT; ++r) {
-      // opaque to the optimiser: keeps it from hoisting 4 d-invariant
-      // addresses per output out of the d loop (register spills)
-      uint32_t v = oab[r];
-      asm volatile("" : "+r"(v));
-      const uint32_t ia = v & 0xffffu, ib = v >> 16;
-      const uint2 la = *reinterpret_cast<const uint2*>(EloB + ia);
-      const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
-      const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
-                          *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
-      const uint64_t c0 = (uint64_t)(lb.x - la.x) + ((uint64_t)(dh & 0xffffu) << kb);
-      const uint64_t c1 = (uint64_t)(lb.y - la.y) + ((uint64_t)(dh >> 16) << kb);
-      best[r] = min(best[r], (c0 << 8) | (uint32_t)d);
-      if (two) best[r] = min(best[r], (c1 << 8) | (uint32_t)(d + 1));
-      if (DBG) {
-        const int yl = seg * kYRPT + r, y = y0 + yl;
-        if (yl < a.B && y < a.Hs && x < a.Ws) {
-          cadbg[((size_t)d * a.Hs + y) * a.Ws + x] = c0;
-          if (two) cadbg[((size_t)(d + 1) * a.Hs + y) * a.Ws + x] = c1;
-        }
-      }
-    }
+    if (d + 1 < Ds)
+      ypass_wta<true, DBG>(best, oab, nr, ysm_elo, ysm_ehi, d, cadbg, a, y0 + seg, x);
+    else
+      ypass_wta<false, DBG>(best, oab, nr, ysm_elo, ysm_ehi, d, cadbg, a, y0 + seg, x);
   }
 #pragma unroll
-  for (int r = 0; r < kYRPT; ++r) {
-    const int yl = seg * kYRPT + r, y = y0 + yl;
-    if (yl < a.B && y < a.Hs && x < a.Ws) dmap[(size_t)y * a.Ws + x] = (uint8_t)(best[r] & 255u);
-  }
+  for (int r = 0; r < kYRPT; ++r)
+    if (r < nr) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(best[r] & 255u);
 }
 
 #define YPASS_DISPATCH(S_, EXPR)                       \
@@ -639,12 +662,7 @@ static int ypass_smem_bytes(int SEG) {
   return kYStages * 2 * TB * 16 * 4 + (TB + 1) * 16 * 12 + 8 * 16 * 16 + kYStages * 8;
 }
 
-// split bit of the two-disparity prefix: (2 w_y + 1) * 2^kb <= 2^32
-static int ypass_split_bits(int w_y) {
-  int lg = 0;
-  while ((1 << lg) < 2 * w_y + 1) ++lg;
-  return lg == 0 ? 31 : 32 - lg;
-}
+
 
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
                          cudaStream_t s) {
@@ -654,7 +672,6 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
-  a.kb = ypass_split_bits(g.w_y);
   dim3 grid((g.Ws + 15) / 16, p.ypass_nb, 2);
   cudaError_t e = cudaErrorInvalidValue;
   if (store_ca)
