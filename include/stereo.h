@@ -174,8 +174,10 @@ int stereo_set_debug(stereo_t* h, int what, int enable);
  * C+CA_x (XPASS) | CA (YPASS) | CC + Post + SU (POST). */
 enum {
   STEREO_STAGE_SD = 0,     /* Eq. 2 (K = 2 only; no-op for K = 1) */
-  STEREO_STAGE_PREP,       /* census + x/y cross arms, both images */
-  STEREO_STAGE_XPASS,      /* C + CA_x, both bases */
+  STEREO_STAGE_PREP,       /* census + x/y cross arms, both images (also writes the
+                              x-pass row arrays, internal, not a debug buffer) */
+  STEREO_STAGE_XPASS,      /* C + CA_x, both bases (reads PREP's internal row
+                              arrays: run PREP first, uploads of PIX/ARM are not seen) */
   STEREO_STAGE_YPASS,      /* CA + WTA, both bases */
   STEREO_STAGE_POST,       /* cross-check + median + bilateral fill + scale-up */
   STEREO_STAGE_COUNT

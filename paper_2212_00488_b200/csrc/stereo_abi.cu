@@ -283,6 +283,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   struct A { void** p; size_t bytes; } as[] = {
       {(void**)&b.pixL, n * 2}, {(void**)&b.pixR, n * 2}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
+      {(void**)&b.xrow, (size_t)4 * g.Hs * g.Wp * 4},
       {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
       {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
       {(void**)&b.patchVals, (size_t)g.Hs * 4},

@@ -29,6 +29,8 @@ struct Buffers {
   uint16_t* pixR = nullptr;
   uint32_t* armL = nullptr;  // m | n<<8 | M<<16 | N<<24
   uint32_t* armR = nullptr;
+  uint32_t* xrow = nullptr;  // u32 [4][Hs][Wp] x-pass rows: code L, code R (census | I << 24),
+                             // window byte offsets L, R (4(x-m) | 4(x+n+1) << 16)
   uint32_t* caxL = nullptr;  // u32 [Ds][Hs][Wp]
   uint32_t* caxR = nullptr;
   uint64_t* caL = nullptr;   // debug only: u64 [Ds][Hs][Ws]
@@ -57,6 +59,7 @@ struct Plan {
   int xpass_grid = 0;
   int xpass_smem = 0;
   int xpass_PL = 0;  // per-warp prefix buffer length
+  int xpass_warps = 0;
   int ypass_B = 0;   // output rows per tile (<= 8*kYRPT)
   int ypass_nb = 0;  // tiles per column strip
   int ypass_SEG = 0; // tile rows per warp; TMA box height = 8*SEG

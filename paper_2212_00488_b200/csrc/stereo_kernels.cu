@@ -13,6 +13,7 @@
 #include <climits>
 #include <cstdio>
 
+#include <algorithm>
 #include "stereo_internal.cuh"
 
 namespace stereo {
@@ -89,7 +90,8 @@ cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const u
 // vcmpgeu4), the run ends at the first dissimilar byte (ffs/clz).
 // Coordinates are clamped on load (census border rule R11); arm scans stop at
 // the real image border (R16).  Output: pix = I | code << 8 (u16),
-// arm = m | n<<8 | M<<16 | N<<24 (u32).
+// arm = m | n<<8 | M<<16 | N<<24 (u32), and the x-pass rows (pitch Wp): code
+// word census | I << 24 and the x-window byte offsets 4(x-m) | 4(x+n+1) << 16.
 // ============================================================================
 struct PrepArgs {
   const uint8_t* img0;
@@ -98,7 +100,8 @@ struct PrepArgs {
   uint16_t* pix1;
   uint32_t* arm0;
   uint32_t* arm1;
-  int Ws, Hs, w_x, w_y, delta;
+  uint32_t* xrow;  // [4][Hs][Wp]: x-pass code L, R; window offsets L, R
+  int Ws, Hs, Wp, w_x, w_y, delta;
   int HX, HY, BWp, AHp;  // halos and padded strip pitches
   int8_t cdx[6], cdy[6];
 };
@@ -172,7 +175,16 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   }
   __syncthreads();
   const int x = x0 + tx, y = y0 + ty;
-  if (x >= a.Ws || y >= a.Hs) return;
+  if (y >= a.Hs) return;
+  const size_t plane = (size_t)a.Hs * a.Wp, ox = (size_t)y * a.Wp + x;
+  uint32_t* xr = a.xrow + blockIdx.z * plane + ox;
+  if (x >= a.Ws) {  // pitch padding of the x-pass rows: harmless windows, never read
+    if (x < a.Wp) {
+      xr[0] = 0u;
+      xr[2 * plane] = 4u * x | (4u * (x + 1)) << 16;
+    }
+    return;
+  }
   const uint8_t* ctr = sB + (ty + 2) * BWp + tx + HX + 8;
   const int c = *ctr;
   int code = 0;
@@ -197,6 +209,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
   (blockIdx.z ? a.arm1 : a.arm0)[o] =
       (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
+  xr[0] = (uint32_t)code | ((uint32_t)c << 24);
+  xr[2 * plane] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
 }
 
 static void prep_geometry(const Geom& g, int& HX, int& HY, int& BWp, int& AHp) {
@@ -213,10 +227,11 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
   a.img0 = Ls; a.img1 = Rs;
   a.pix0 = b.pixL; a.pix1 = b.pixR;
   a.arm0 = b.armL; a.arm1 = b.armR;
-  a.Ws = g.Ws; a.Hs = g.Hs; a.w_x = g.w_x; a.w_y = g.w_y; a.delta = g.delta;
+  a.xrow = b.xrow;
+  a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_y = g.w_y; a.delta = g.delta;
   prep_geometry(g, a.HX, a.HY, a.BWp, a.AHp);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
-  dim3 grid((g.Ws + 31) / 32, (g.Hs + 7) / 8, 2);
+  dim3 grid(g.Wp / 32, (g.Hs + 7) / 8, 2);
   prep_kernel<<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -230,21 +245,29 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
 //        CA^R_x(x,d) = P[x+d+n_R+1] - P[x+d-m_R]
 // with P extended by BORDER = 2^(f+1) per column beyond Ws, replacing
 // the paper's O(W_x) direct sums by O(1) differences.
-// Work unit = (row y, 16 consecutive d); each warp owns one d at a time:
+// Persistent: one CTA per SM owns a contiguous range of work items
+// (row y, disparity group of ND); every warp takes items independently.  The
+// four PREP row arrays of a row (codes, window offsets; pitch Wp) arrive by
+// bulk asynchronous copies into a ring of kXSlots row slots, completed on an
+// mbarrier; the warp that finishes the last item of a row in the range
+// refills its slot with the row kXSlots ahead, so row loads overlap compute
+// and no CTA-wide barrier is needed after the start.  Per item:
 //   phase A: lane l scans its contiguous chunk [lC, lC+C) (C odd -> shared
 //            loads at stride C are bank-conflict free); costs from the fixed
 //            tables Q_AD[|dI|] and Q_MC[cL ^ cR] (popc folded into a 64-entry
 //            table), both replicated per bank (index*32 + lane); branch-free
 //            BORDER select for x < d;
 //   warp scan of the 32 lane totals (shuffles) -> P into shared memory;
-//   phase C: lanes interleaved over x -> two coalesced 128-B stores per warp.
-// Output layout: u32 [Ds][Hs][Wp] (Wp = Ws rounded up to 32).
+//   phase C: lanes interleaved over x -> two coalesced 128-B stores per warp
+//            and disparity.
+// ND = 2: two consecutive disparities d, d+1 per item.  The right pixel of
+// (x, d+1) is the one of (x-1, d), so both cost rows come from the same C + 1
+// shared loads per lane, both window sets from the same offsets, and the two
+// shuffle scans overlap.
+// Output layout: u32 [Ds][Hs][Wp] (Wp = 32C).
 // ============================================================================
 struct XArgs {
-  const uint16_t* pixL;
-  const uint16_t* pixR;
-  const uint32_t* armL;
-  const uint32_t* armR;
+  const uint32_t* xrow;  // [4][Hs][Wp]
   const uint32_t* qad;
   const uint32_t* qmc;
   uint32_t* caxL;
@@ -253,98 +276,184 @@ struct XArgs {
   uint32_t border;
 };
 
-constexpr int kXWarps = 8;
-constexpr int kXDPerUnit = 16;
+constexpr int kXMaxWarps = 16;
+constexpr int kXSlots = 3;
 
-template <int C>
-__global__ void __launch_bounds__(kXWarps * 32, 2) xpass_kernel(XArgs a) {
-  extern __shared__ uint32_t xsm[];
-  uint32_t* sQAD = xsm;              // [256][32]  Q_AD[|dI|], one copy per bank
-  uint32_t* sQMC = sQAD + 256 * 32;  // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
-  uint32_t* sL = sQMC + 64 * 32;     // [32C] left row:  census | I << 24
-  uint32_t* sR = sL + 32 * C;        // [32C] right row: census | I << 24
-  uint32_t* sAL = sR + 32 * C;       // [32C] byte offsets 4(x-m_L) | 4(x+n_L+1) << 16
-  uint32_t* sAR = sAL + 32 * C;      // [32C] byte offsets 4(x-m_R) | 4(x+n_R+1) << 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void xbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void xbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "XWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra XWAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one row's four arrays into a slot (single thread)
+__device__ __forceinline__ void xpass_load_row(uint32_t* slot, uint64_t* bar, const XArgs& a,
+                                               int row) {
+  const uint32_t bytes = (uint32_t)a.Wp * 4u;
+  const size_t plane = (size_t)a.Hs * a.Wp;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(4u * bytes)
+               : "memory");
+  for (int k = 0; k < 4; ++k)
+    bulk_g2s(slot + k * a.Wp, a.xrow + k * plane + (size_t)row * a.Wp, bytes, bar);
+}
+
+template <int C, int ND>
+__global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
+  static_assert(ND == 1 || ND == 2, "one or two disparities per item");
+  extern __shared__ __align__(128) uint32_t xsm[];
+  uint32_t* sQAD = xsm;                // [256][32]  Q_AD[|dI|], one copy per bank
+  uint32_t* sQMC = sQAD + 256 * 32;    // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
+  uint32_t* ring = sQMC + 64 * 32;     // [kXSlots][4][32C] row slots
+  const int nw = blockDim.x >> 5;
+  uint32_t* Pall = ring + kXSlots * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * a.PL);  // [kXSlots]
+  unsigned* done = reinterpret_cast<unsigned*>(full + kXSlots);                // [kXSlots]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* P = sAR + 32 * C + warp * a.PL;  // [PL] exclusive prefix (+ BORDER extension)
+  uint32_t* P = Pall + warp * ND * a.PL;
 
+  // this CTA's item range [i0, i1) of the Hs * npairs items, and its rows
+  const int npairs = (a.Ds + ND - 1) / ND;
+  const long long total = (long long)a.Hs * npairs;
+  const int i0 = (int)(total * blockIdx.x / gridDim.x);
+  const int i1 = (int)(total * (blockIdx.x + 1) / gridDim.x);
+  if (i0 >= i1) return;
+  const int rfirst = i0 / npairs, rlast = (i1 - 1) / npairs;
+  const int skip0 = i0 - rfirst * npairs;  // items of the first row owned by earlier CTAs
+
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kXSlots; ++k) {
+      xbar_init(full + k);
+      done[k] = 0u;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < kXSlots && rfirst + k <= rlast; ++k)
+      xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
+  }
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sQAD[i] = __ldg(a.qad + (i >> 5));
   for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) sQMC[i] = __ldg(a.qmc + __popc(i >> 5));
+  __syncthreads();
   // with pixels encoded as census | I << 24, |dI|*128 = vabsdiffu4(pl, pr) >> 17 and
   // (cL ^ cR)*128 = ((pl ^ pr) & 63) << 7: table addresses in two ALU operations.
   const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
   const char* qmcb = reinterpret_cast<const char*>(sQMC + lane);
   const char* Pb = reinterpret_cast<const char*>(P);
-
-  const int nch = (a.Ds + kXDPerUnit - 1) / kXDPerUnit;
-  const int units = a.Hs * nch;
+  const int PLb = 4 * a.PL;
   const int Ws = a.Ws;
   const uint32_t border = a.border;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const int y = u / nch, d0 = (u - y * nch) * kXDPerUnit;
-    __syncthreads();  // previous unit finished with the row buffers
-    for (int x = threadIdx.x; x < 32 * C; x += blockDim.x) {
-      uint32_t l = 0, r = 0, al = 4u * x | (4u * (x + 1)) << 16, ar = al;
-      if (x < Ws) {
-        const size_t o = (size_t)y * Ws + x;
-        const uint32_t pl = __ldg(a.pixL + o), pr = __ldg(a.pixR + o);
-        l = (pl >> 8) | (pl << 24);
-        r = (pr >> 8) | (pr << 24);
-        const uint32_t aL = __ldg(a.armL + o), aR = __ldg(a.armR + o);
-        al = 4u * (x - (aL & 255u)) | (4u * (x + ((aL >> 8) & 255u) + 1)) << 16;
-        ar = 4u * (x - (aR & 255u)) | (4u * (x + ((aR >> 8) & 255u) + 1)) << 16;
-      }
-      sL[x] = l; sR[x] = r; sAL[x] = al; sAR[x] = ar;
-    }
-    __syncthreads();
+
 #pragma unroll 1
-    for (int j = 0; j < kXDPerUnit / kXWarps; ++j) {
-      const int d = d0 + j * kXWarps + warp;
-      if (d >= a.Ds) break;
-      // ---- phase A: costs of the lane's chunk + local inclusive prefix
-      const uint32_t* Lr = sL + lane * C;
-      const uint32_t* Rr = sR + lane * C - d;  // may point before sR: those lanes take BORDER
-      const int nb = d - lane * C;             // elements k < nb have x - d < 0
-      uint32_t pref[C];
-      uint32_t run = 0;
+  for (int it = i0 + warp; it < i1; it += nw) {
+    const int y = it / npairs, d = (it - y * npairs) * ND;
+    const int rel = y - rfirst, slot = rel % kXSlots;
+    xbar_wait(full + slot, (uint32_t)(rel / kXSlots) & 1u);
+    const uint32_t* sL = ring + slot * 4 * 32 * C;
+    const uint32_t* sR = sL + 32 * C;
+    const uint32_t* sAL = sR + 32 * C;
+    const uint32_t* sAR = sAL + 32 * C;
+    const bool two = ND == 2 && d + 1 < a.Ds;
+    // ---- phase A: costs of the lane's chunk + local inclusive prefixes
+    const uint32_t* Lr = sL + lane * C;
+    // elements k < nb have x - d < 0 and take BORDER; their loads land before
+    // sR (in the slot's sL or the tables: d <= 255) and are unused
+    const int nb = d - lane * C;
+    const uint32_t* Rr = sR + lane * C - d;
+    uint32_t pref[ND][C];
+    uint32_t run[ND] = {};
+    uint32_t prv = ND == 2 ? Rr[-1] : 0u;  // right pixel of (x, d+1) = of (x-1, d)
 #pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const uint32_t pl = Lr[k], pr = Rr[k];
-        const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
-        const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & 63u) << 7));
-        run += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
-        pref[k] = run;
+    for (int k = 0; k < C; ++k) {
+      const uint32_t pl = Lr[k], pr = Rr[k];
+      const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
+      const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & 63u) << 7));
+      run[0] += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
+      pref[0][k] = run[0];
+      if (ND == 2) {
+        const uint32_t qa1 = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, prv) >> 17));
+        const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & 63u) << 7));
+        run[ND - 1] += (k < nb + 1) ? border : qa1 + qm1;
+        pref[ND - 1][k] = run[ND - 1];
+        prv = pr;
       }
-      uint32_t incl = run;
+    }
+    uint32_t incl[ND];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
+    for (int n = 0; n < ND; ++n) incl[n] = run[n];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int n = 0; n < ND; ++n) {
+        const uint32_t t = __shfl_up_sync(kFull, incl[n], o);
+        if (lane >= o) incl[n] += t;
       }
-      const uint32_t off = incl - run;
-      uint32_t* Pl = P + lane * C + 1;
+    }
 #pragma unroll
-      for (int k = 0; k < C; ++k) Pl[k] = pref[k] + off;
-      if (lane == 0) P[0] = 0;
-      __syncwarp();
-      const uint32_t PW = P[Ws];
-      for (int e = lane; e < a.ext; e += 32) P[Ws + 1 + e] = PW + (uint32_t)(e + 1) * border;
-      __syncwarp();
-      // ---- phase C: window differences (precomputed byte offsets), coalesced stores
-      uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp + lane;
-      uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp + lane;
-      const char* Pdb = Pb + 4 * d;
+    for (int n = 0; n < ND; ++n) {
+      const uint32_t off = incl[n] - run[n];
+      uint32_t* Pl = P + n * a.PL + lane * C + 1;
 #pragma unroll
-      for (int i = 0; i < C; ++i) {
-        const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
-        const uint32_t caL = *reinterpret_cast<const uint32_t*>(Pb + (al >> 16)) -
-                             *reinterpret_cast<const uint32_t*>(Pb + (al & 0xffffu));
-        const uint32_t caR = *reinterpret_cast<const uint32_t*>(Pdb + (ar >> 16)) -
-                             *reinterpret_cast<const uint32_t*>(Pdb + (ar & 0xffffu));
-        outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
-        outR[32 * i] = caR;
+      for (int k = 0; k < C; ++k) Pl[k] = pref[n][k] + off;
+    }
+    if (lane < ND) P[lane * a.PL] = 0;
+    __syncwarp();
+    uint32_t PW[ND];
+#pragma unroll
+    for (int n = 0; n < ND; ++n) PW[n] = P[n * a.PL + Ws];
+    for (int e = lane; e < a.ext; e += 32) {
+#pragma unroll
+      for (int n = 0; n < ND; ++n) P[n * a.PL + Ws + 1 + e] = PW[n] + (uint32_t)(e + 1) * border;
+    }
+    __syncwarp();
+    // ---- phase C: window differences (precomputed byte offsets), coalesced stores
+    uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp + lane;
+    uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp + lane;
+    const size_t dstep = (size_t)a.Hs * a.Wp;
+    const char* Pdb = Pb + 4 * d;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
+      const uint32_t alo = al & 0xffffu, ahi = al >> 16, arlo = ar & 0xffffu, arhi = ar >> 16;
+      const uint32_t caL = *reinterpret_cast<const uint32_t*>(Pb + ahi) -
+                           *reinterpret_cast<const uint32_t*>(Pb + alo);
+      const uint32_t caR = *reinterpret_cast<const uint32_t*>(Pdb + arhi) -
+                           *reinterpret_cast<const uint32_t*>(Pdb + arlo);
+      outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
+      outR[32 * i] = caR;
+      if (ND == 2 && two) {
+        const char* P1 = Pb + PLb;
+        const char* P1d = Pdb + PLb + 4;
+        const uint32_t caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) -
+                              *reinterpret_cast<const uint32_t*>(P1 + alo);
+        const uint32_t caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) -
+                              *reinterpret_cast<const uint32_t*>(P1d + arlo);
+        outL[dstep + 32 * i] = caL1;
+        outR[dstep + 32 * i] = caR1;
       }
-      __syncwarp();
+    }
+    __syncwarp();
+    // ---- release the row slot: the warp finishing the row's last item of
+    // this range refills the slot with the row kXSlots ahead
+    if (lane == 0) {
+      __threadfence_block();
+      const unsigned target = (unsigned)((rel / kXSlots + 1) * npairs - (slot == 0 ? skip0 : 0));
+      const unsigned prev = atomicAdd(done + slot, 1u);
+      if (prev + 1u == target && y + kXSlots <= rlast) {
+        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + kXSlots);
+      }
     }
   }
 }
@@ -355,24 +464,23 @@ int xpass_chunk_for(int Ws) {
   return 0;
 }
 
+// two disparities per item while the 2C prefix registers fit
+constexpr int kXMaxC2 = 27;
+template <int C>
+constexpr int xpass_nd() { return C <= kXMaxC2 ? 2 : 1; }
+
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
-  XArgs a{b.pixL, b.pixR, b.armL, b.armR, b.qad, b.qmc, b.caxL, b.caxR,
+  XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
           g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x, g.border};
-  xpass_kernel<C><<<p.xpass_grid, kXWarps * 32, p.xpass_smem, s>>>(a);
+  xpass_kernel<C, xpass_nd<C>()><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int C>
 static cudaError_t setup_xpass_c(int smem) {
-  return cudaFuncSetAttribute(xpass_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-}
-
-template <int C>
-static int occ_xpass_c(int smem) {
-  int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, xpass_kernel<C>, kXWarps * 32, smem);
-  return n;
+  return cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>()>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 #define XPASS_DISPATCH(C_, EXPR)                        \
@@ -1128,18 +1236,24 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     }
     if (e != cudaSuccess) return e;
   }
-  // XPASS
+  // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
   p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x + 3;
-  p.xpass_smem = (int)(sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + 4 * 32 * p.xpass_C +
-                                           (size_t)kXWarps * p.xpass_PL));
-  int occ = 0;
-  XPASS_DISPATCH(p.xpass_C, (e = setup_xpass_c<CC>(p.xpass_smem), occ = occ_xpass_c<CC>(p.xpass_smem)));
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  const int units = g.Hs * ((g.Ds + kXDPerUnit - 1) / kXDPerUnit);
-  p.xpass_grid = units < occ * nsm ? units : occ * nsm;
+  {
+    const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
+    const size_t fixed = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 +
+                                             (size_t)kXSlots * 4 * 32 * p.xpass_C) +
+                         kXSlots * (8 + 4);
+    const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
+    const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
+    if (fixed + per_warp > cap) return cudaErrorInvalidConfiguration;
+    p.xpass_warps = (int)std::min<size_t>(kXMaxWarps, (cap - fixed) / per_warp);
+    p.xpass_smem = (int)(fixed + per_warp * p.xpass_warps);
+    XPASS_DISPATCH(p.xpass_C, e = setup_xpass_c<CC>(p.xpass_smem));
+    if (e != cudaSuccess) return e;
+    p.xpass_grid = nsm;
+  }
   // YPASS: choose the number of tiles per strip balancing halo cost and waves
   // (per-CTA shared wavefronts per d ~ 1.25*TB + 1.75*B + tot exchange)
   const int strips = (g.Ws + 15) / 16;
