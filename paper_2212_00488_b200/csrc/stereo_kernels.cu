@@ -599,39 +599,61 @@ constexpr int kYSplit = 24;
 
 template <bool DBG>
 __device__ __forceinline__ void ypass_take(uint64_t& best, uint32_t lo, uint32_t hi, int d,
-                                           uint64_t* cadbg, size_t dbg_idx) {
+                                           uint64_t* cadbg, size_t dbg_idx, bool live) {
   const uint32_t klo = (lo << 8) | (uint32_t)d;
   const uint32_t khi = (lo >> 24) + hi;
   const uint64_t key = ((uint64_t)khi << 32) | klo;
   best = min(best, key);
-  if (DBG && cadbg) cadbg[dbg_idx] = key >> 8;
+  if (DBG && live) cadbg[dbg_idx] = key >> 8;
 }
 
-// WTA over the window sums of d (and d+1 if TWO) for the thread's outputs.
-template <bool TWO, bool DBG>
+// WTA over the window sums of d (and d+1 if TWO) for the thread's outputs
+// r < NR (NR warp-uniform: straight-line code the scheduler can interleave).
+// `z` is an opaque per-iteration zero: it keeps the optimiser from hoisting
+// four d-invariant addresses per output out of the d loop (register spills).
+template <int NR, bool TWO, bool DBG>
 __device__ __forceinline__ void ypass_wta(uint64_t (&best)[kYRPT], const uint32_t (&oab)[kYRPT],
-                                          int nr, uint32_t elo, uint32_t ehi, int d,
-                                          uint64_t* cadbg, const YArgs& a, int yrow0, int x) {
+                                          const uint8_t* EloB, const uint8_t* EhiB, uint32_t z,
+                                          int d, uint64_t* cadbg, const YArgs& a, int yrow0,
+                                          int x) {
 #pragma unroll
-  for (int r = 0; r < kYRPT; ++r) {
-    if (r < nr) {
-      // opaque to the optimiser: keeps it from hoisting 4 d-invariant
-      // addresses per output out of the d loop (register spills)
-      uint32_t v = oab[r];
-      asm volatile("" : "+r"(v));
-      const uint32_t ia = v & 0xffffu, ib = v >> 16;
-      uint32_t la0, la1, lb0, lb1, ha, hb;
-      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(la0), "=r"(la1) : "r"(elo + ia));
-      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lb0), "=r"(lb1) : "r"(elo + ib));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ha) : "r"(ehi + (ia >> 1)));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hb) : "r"(ehi + (ib >> 1)));
-      const uint32_t dh = hb - ha;
-      const size_t di = DBG ? ((size_t)d * a.Hs + yrow0 + 16 * r) * a.Ws + x : 0;
-      ypass_take<DBG>(best[r], lb0 - la0, dh & 0xffffu, d, cadbg, di);
-      if (TWO)
-        ypass_take<DBG>(best[r], lb1 - la1, dh >> 16, d + 1, cadbg,
-                        di + (DBG ? (size_t)a.Hs * a.Ws : 0));
-    }
+  for (int r = 0; r < NR; ++r) {
+    const uint32_t v = oab[r] + z;
+    const uint32_t ia = v & 0xffffu, ib = v >> 16;
+    const uint2 la = *reinterpret_cast<const uint2*>(EloB + ia);
+    const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
+    const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
+                        *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
+    const bool live = !DBG || (yrow0 + 16 * r < a.Hs && x < a.Ws);
+    const size_t di = DBG ? ((size_t)d * a.Hs + yrow0 + 16 * r) * a.Ws + x : 0;
+    ypass_take<DBG>(best[r], lb.x - la.x, dh & 0xffffu, d, cadbg, di, live);
+    if (TWO)
+      ypass_take<DBG>(best[r], lb.y - la.y, dh >> 16, d + 1, cadbg,
+                      di + (DBG ? (size_t)a.Hs * a.Ws : 0), live);
+  }
+}
+
+template <bool TWO, bool DBG>
+__device__ __forceinline__ void ypass_wta_n(int nr, uint64_t (&best)[kYRPT],
+                                            const uint32_t (&oab)[kYRPT], const uint8_t* EloB,
+                                            const uint8_t* EhiB, int d, uint64_t* cadbg,
+                                            const YArgs& a, int yrow0, int x) {
+  uint32_t z;
+  asm volatile("mov.u32 %0, 0;" : "=r"(z));
+  switch (nr) {  // warp-uniform (depends on the row segment only)
+    case 12: ypass_wta<12, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 11: ypass_wta<11, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 10: ypass_wta<10, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 9: ypass_wta<9, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 8: ypass_wta<8, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 7: ypass_wta<7, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 6: ypass_wta<6, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 5: ypass_wta<5, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 4: ypass_wta<4, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 3: ypass_wta<3, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 2: ypass_wta<2, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 1: ypass_wta<1, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    default: break;
   }
 }
 
@@ -661,7 +683,10 @@ __global__ void __launch_bounds__(kYThreads, 2)
   // output rows of this thread: y0 + seg + 16 r, r < nr (interleaved, so the
   // rows past B are whole trailing iterations, mostly warp-uniform)
   const int nrow = min(a.B, a.Hs - y0);
-  const int nr = x < a.Ws ? max(0, (nrow - seg + 15) >> 4) : 0;
+  const int nr = max(0, (nrow - seg + 15) >> 4);  // same for both segments of a warp if B even
+  // (B odd: the two half-warps may differ by one row; the warp then runs the
+  // larger count and the extra row reads a harmless window, never stored)
+  const int nrw = max(nr, __shfl_xor_sync(kFull, nr, 16));
 
   if (tid == 0) {
     for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
@@ -688,14 +713,15 @@ __global__ void __launch_bounds__(kYThreads, 2)
     const int y = y0 + seg + 16 * r;
     oab[r] = 0u;
     best[r] = ~0ull;
-    if (r < nr) {
+    if (r < nr && x < a.Ws) {
       const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
       const int M = (arm >> 16) & 255u, N = arm >> 24;
       oab[r] = (((uint32_t)(y - M - yt0) * 16u + col) * 8u) |
                ((((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u) << 16);
     }
   }
-  const uint32_t ysm_elo = smem_u32(Elo), ysm_ehi = smem_u32(Ehi);
+  const uint8_t* EloB = reinterpret_cast<const uint8_t*>(Elo);
+  const uint8_t* EhiB = reinterpret_cast<const uint8_t*>(Ehi);
   uint2* Ew = Elo + (seg * SEG + 1) * 16 + col;
   uint32_t* Hw = Ehi + (seg * SEG + 1) * 16 + col;
   constexpr uint32_t kLoMask = (1u << kYSplit) - 1u;
@@ -738,13 +764,13 @@ __global__ void __launch_bounds__(kYThreads, 2)
     }
     __syncthreads();  // (2) column prefixes complete
     if (d + 1 < Ds)
-      ypass_wta<true, DBG>(best, oab, nr, ysm_elo, ysm_ehi, d, cadbg, a, y0 + seg, x);
+      ypass_wta_n<true, DBG>(nrw, best, oab, EloB, EhiB, d, cadbg, a, y0 + seg, x);
     else
-      ypass_wta<false, DBG>(best, oab, nr, ysm_elo, ysm_ehi, d, cadbg, a, y0 + seg, x);
+      ypass_wta_n<false, DBG>(nrw, best, oab, EloB, EhiB, d, cadbg, a, y0 + seg, x);
   }
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r)
-    if (r < nr) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(best[r] & 255u);
+    if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(best[r] & 255u);
 }
 
 #define YPASS_DISPATCH(S_, EXPR)                       \
