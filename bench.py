@@ -270,39 +270,40 @@ def run_ours(args):
     fps = ws * args.steps / (ms_max / 1e3)
 
     # ---- end to end through the public C ABI with HOST buffers (pinned):
-    # H2D of L, R + compute + D2H of the disparity map, every step, two
-    # streams / two handles so copies overlap the previous frame's kernels.
-    st2 = abi.Stereo(W, H, D) if NS < 2 else handles[1]
-    e2e_h = (st, st2)
-    e2e_s = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    # H2D of L, R + compute + D2H of the disparity map, every step, on the same
+    # number of streams / handles as the device-resident run (at least two) so
+    # the copies overlap other frames' kernels.
+    NE = max(NS, 2)
+    extra = [abi.Stereo(W, H, D) for _ in range(NE - NS)]
+    e2e_h = list(handles) + extra
+    e2e_s = [torch.cuda.Stream(dev) for _ in range(NE)]
     nh = 8
     Lh = [torch.from_numpy(frames[i][0]).pin_memory() for i in range(nh)]
     Rh = [torch.from_numpy(frames[i][1]).pin_memory() for i in range(nh)]
     Oh = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in range(nh)]
     e2e_steps = max(args.steps // 4, 8)
-    for i in range(4):
-        e2e_h[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i & 1])
+    for i in range(2 * NE):
+        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i % NE])
     torch.cuda.synchronize()
     barrier()
-    ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ea = [torch.cuda.Event(enable_timing=True) for _ in range(NE)]
+    eb = [torch.cuda.Event(enable_timing=True) for _ in range(NE)]
     t0 = time.perf_counter()
-    for s_ in range(2):
+    for s_ in range(NE):
         ea[s_].record(e2e_s[s_])
     for i in range(e2e_steps):
-        e2e_h[i & 1].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i & 1])
-    for s_ in range(2):
+        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i % NE])
+    for s_ in range(NE):
         eb[s_].record(e2e_s[s_])
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    e2e_ms = max(ea[0].elapsed_time(eb[0]), ea[1].elapsed_time(eb[1]),
-                 ea[0].elapsed_time(eb[1]), ea[1].elapsed_time(eb[0]))
+    e2e_ms = max(ea[i].elapsed_time(eb[j]) for i in range(NE) for j in range(NE))
     t2 = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_fps = ws * e2e_steps / (float(t2.item()) / 1e3)
-    if NS < 2:
-        st2.close()
+    for h_ in extra:
+        h_.close()
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -349,7 +350,7 @@ def run_ours(args):
             "e2e": {"value": e2e_fps, "unit": "fps", "h2d_bytes_per_step": 2 * W * H,
                     "d2h_bytes_per_step": 4 * W * H, "steps": e2e_steps,
                     "how": "stereo_compute_host (pinned host L/R -> device, compute, device -> host "
-                           "f32 map), 2 handles on 2 streams", "wall_s": wall},
+                           f"f32 map), {NE} handles on {NE} streams", "wall_s": wall},
             "gpu_launches": args.steps * info.launches_per_frame,
             "clocks": clk.summary(),
         }

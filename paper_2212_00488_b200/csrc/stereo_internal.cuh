@@ -66,8 +66,11 @@ struct Plan {
   int ypass_smem = 0;
   CUtensorMap tmL, tmR;  // 3-D maps over the CA_x volumes {Wp, Hs, Ds}
   int post_smem = 0;
+  int post_rows = 2;     // scaled rows per POST CTA
+  int post_threads = 512;
   int sd_smem = 0;
   int prep_smem = 0;
+  int prep_rows = 1;  // pixel rows per PREP thread (tile 32 x 8*prep_rows)
 };
 
 // Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch error.

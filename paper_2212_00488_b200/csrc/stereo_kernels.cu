@@ -12,6 +12,7 @@
 // round-to-nearest intrinsics (no FMA contraction) for the fill and scale-up.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include "stereo_internal.cuh"
@@ -82,7 +83,7 @@ cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const u
 // ============================================================================
 // PREP — mini-census (Fig. 3; pattern is a parameter, reading R8)
 // and the four cross arms (Steps 2 and 4)
-// of both scaled images.  A 32x8 pixel tile is staged in shared memory as a
+// of both scaled images.  A 32x32 pixel tile (4 rows per thread) is staged in shared memory as a
 // horizontal strip (rows +-2, cols +-max(w_x,2)) for the census and the x
 // arms and a TRANSPOSED vertical strip (cols +-2, rows +-max(w_y,2)) for the
 // y arms, so that both arm scans read contiguous bytes: 4 neighbours are
@@ -149,15 +150,21 @@ __device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint
   }
 }
 
+// PR pixel rows per thread: tile 32 x 8PR pixels (taller tiles amortise the
+// vertical halo of the y-arm strip; the plan picks PR by grid size)
+template <int PR>
 __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
+  constexpr int kPrepRows = PR;
+  constexpr int kPrepTH = 8 * PR;       // tile height
+  constexpr int kPrepSB = kPrepTH + 4;  // rows of the horizontal strip
   extern __shared__ uint32_t psm32[];
-  uint8_t* sB = reinterpret_cast<uint8_t*>(psm32);  // [12][BWp]  horizontal strip
-  uint8_t* sV = sB + 12 * a.BWp;                      // [36][AHp]  vertical strip, transposed
+  uint8_t* sB = reinterpret_cast<uint8_t*>(psm32);  // [kPrepSB][BWp]  horizontal strip
+  uint8_t* sV = sB + kPrepSB * a.BWp;                 // [36][AHp]  vertical strip, transposed
   const uint8_t* img = blockIdx.z ? a.img1 : a.img0;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * kPrepTH;
   const int HX = a.HX, HY = a.HY, BWp = a.BWp, AHp = a.AHp;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int r = ty; r < 12; r += 8) {
+  for (int r = ty; r < kPrepSB; r += 8) {
     const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws;
     for (int c = tx; c < BWp; c += 32) sB[r * BWp + c] = __ldg(row + clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
   }
@@ -174,50 +181,60 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     }
   }
   __syncthreads();
-  const int x = x0 + tx, y = y0 + ty;
-  if (y >= a.Hs) return;
-  const size_t plane = (size_t)a.Hs * a.Wp, ox = (size_t)y * a.Wp + x;
-  uint32_t* xr = a.xrow + blockIdx.z * plane + ox;
-  if (x >= a.Ws) {  // pitch padding of the x-pass rows: harmless windows, never read
-    if (x < a.Wp) {
-      xr[0] = 0u;
-      xr[2 * plane] = 4u * x | (4u * (x + 1)) << 16;
+  const int x = x0 + tx;
+  const size_t plane = (size_t)a.Hs * a.Wp;
+  const bool big = a.delta >= 128;
+  const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
+#pragma unroll 1
+  for (int rr = 0; rr < kPrepRows; ++rr) {
+    const int ty2 = ty + 8 * rr, y = y0 + ty2;
+    if (y >= a.Hs) return;
+    uint32_t* xr = a.xrow + blockIdx.z * plane + (size_t)y * a.Wp + x;
+    if (x >= a.Ws) {  // pitch padding of the x-pass rows: harmless windows, never read
+      if (x < a.Wp) {
+        xr[0] = 0u;
+        xr[2 * plane] = 4u * x | (4u * (x + 1)) << 16;
+      }
+      continue;
     }
-    return;
-  }
-  const uint8_t* ctr = sB + (ty + 2) * BWp + tx + HX + 8;
-  const int c = *ctr;
-  int code = 0;
+    const uint8_t* ctr = sB + (ty2 + 2) * BWp + tx + HX + 8;
+    const int c = *ctr;
+    int code = 0;
 #pragma unroll
-  for (int i = 0; i < 6; ++i) code |= (ctr[a.cdy[i] * BWp + a.cdx[i]] < c) << i;
-  int n, m, N, M;
-  if (a.delta > 255) {  // |dI| <= 255 < delta: every neighbour is similar
-    n = min(a.w_x, a.Ws - 1 - x); m = min(a.w_x, x);
-    N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
-  } else {
-    const bool big = a.delta >= 128;
-    const uint32_t c4 = (uint32_t)c * 0x01010101u;
-    const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
-    const int oB = (ty + 2) * BWp + tx + HX + 8;                 // centre in sB
-    const int oV = 12 * BWp + (tx + 2) * AHp + ty + HY + 8;      // centre in sV
-    n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, dl4, big);
-    m = run_bwd(psm32, oB, min(a.w_x, x), c4, dl4, big);
-    N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, dl4, big);
-    M = run_bwd(psm32, oV, min(a.w_y, y), c4, dl4, big);
+    for (int i = 0; i < 6; ++i) code |= (ctr[a.cdy[i] * BWp + a.cdx[i]] < c) << i;
+    int n, m, N, M;
+    if (a.delta > 255) {  // |dI| <= 255 < delta: every neighbour is similar
+      n = min(a.w_x, a.Ws - 1 - x); m = min(a.w_x, x);
+      N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
+    } else {
+      const uint32_t c4 = (uint32_t)c * 0x01010101u;
+      const int oB = (ty2 + 2) * BWp + tx + HX + 8;                      // centre in sB
+      const int oV = kPrepSB * BWp + (tx + 2) * AHp + ty2 + HY + 8;      // centre in sV
+      n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, dl4, big);
+      m = run_bwd(psm32, oB, min(a.w_x, x), c4, dl4, big);
+      N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, dl4, big);
+      M = run_bwd(psm32, oV, min(a.w_y, y), c4, dl4, big);
+    }
+    const size_t o = (size_t)y * a.Ws + x;
+    (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
+    (blockIdx.z ? a.arm1 : a.arm0)[o] =
+        (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
+    xr[0] = (uint32_t)code | ((uint32_t)c << 24);
+    xr[2 * plane] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
   }
-  const size_t o = (size_t)y * a.Ws + x;
-  (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
-  (blockIdx.z ? a.arm1 : a.arm0)[o] =
-      (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
-  xr[0] = (uint32_t)code | ((uint32_t)c << 24);
-  xr[2 * plane] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
 }
 
-static void prep_geometry(const Geom& g, int& HX, int& HY, int& BWp, int& AHp) {
+static int prep_rows_for(const Geom& g, int nsm) {
+  for (int pr : {4, 2})
+    if ((long long)(g.Wp / 32) * ((g.Hs + 8 * pr - 1) / (8 * pr)) * 2 >= 4LL * nsm) return pr;
+  return 1;
+}
+
+static void prep_geometry(const Geom& g, int pr, int& HX, int& HY, int& BWp, int& AHp) {
   HX = g.w_x > 2 ? g.w_x : 2;
   HY = g.w_y > 2 ? g.w_y : 2;
   BWp = (32 + 2 * HX + 16 + 15) & ~15;
-  AHp = (8 + 2 * HY + 16 + 3) & ~3;
+  AHp = (8 * pr + 2 * HY + 16 + 3) & ~3;
   if (((AHp >> 2) & 1) == 0) AHp += 4;  // odd word pitch: conflict-free transposed stores
 }
 
@@ -229,10 +246,13 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
   a.arm0 = b.armL; a.arm1 = b.armR;
   a.xrow = b.xrow;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_y = g.w_y; a.delta = g.delta;
-  prep_geometry(g, a.HX, a.HY, a.BWp, a.AHp);
+  const int pr = p.prep_rows;
+  prep_geometry(g, pr, a.HX, a.HY, a.BWp, a.AHp);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
-  dim3 grid(g.Wp / 32, (g.Hs + 7) / 8, 2);
-  prep_kernel<<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
+  dim3 grid(g.Wp / 32, (g.Hs + 8 * pr - 1) / (8 * pr), 2);
+  if (pr == 4) prep_kernel<4><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
+  else if (pr == 2) prep_kernel<2><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
+  else prep_kernel<1><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -926,11 +946,9 @@ __device__ void su_row_global(const PostArgs& a, int Y, float thr) {
   }
 }
 
-constexpr int kPostRows = 2;  // scaled rows owned per CTA
-
+template <int R>  // scaled rows owned per CTA
 __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   extern __shared__ uint32_t psm_[];
-  constexpr int R = kPostRows;
   const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5, W = a.W, Wx = a.Wx;
   uint8_t* mk = reinterpret_cast<uint8_t*>(psm_);                  // [R+3][Wsp] masked rows
   uint8_t* md = mk + (R + 3) * Wsp;                                // [R+1][Wsp] median rows
@@ -1200,7 +1218,10 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.Wsp = (g.Ws + 31) & ~31;
   a.Wx = (g.W + 3) & ~3;
-  post_kernel<<<(g.Hs + kPostRows - 1) / kPostRows, 512, p.post_smem, s>>>(a);
+  const int R = p.post_rows, nt = p.post_threads;
+  if (R == 1) post_kernel<1><<<g.Hs, nt, p.post_smem, s>>>(a);
+  else if (R == 2) post_kernel<2><<<(g.Hs + 1) / 2, nt, p.post_smem, s>>>(a);
+  else post_kernel<4><<<(g.Hs + 3) / 4, nt, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1242,17 +1263,25 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   p.sd_smem = (2 * g.m_pool + 1) * ((g.W + 3) & ~3) + 16;
   {
     int HX, HY, BWp, AHp;
-    prep_geometry(g, HX, HY, BWp, AHp);
-    p.prep_smem = 12 * BWp + 36 * AHp + 16;
+    p.prep_rows = prep_rows_for(g, nsm);
+    prep_geometry(g, p.prep_rows, HX, HY, BWp, AHp);
+    p.prep_smem = (8 * p.prep_rows + 4) * BWp + 36 * AHp + 16;
   }
   const int Wsp = (g.Ws + 31) & ~31;
   const int Wx = (g.W + 3) & ~3;
-  p.post_smem = (kPostRows + 3) * Wsp + (kPostRows + 1) * Wsp + (kPostRows + 1) * Wsp * 4 +
-                (kPostRows + 1) * Wx * 4 + 3 * (kPostRows + 1) * 64 * 4 +
-                (kPostRows + 1) * Wsp * 2 + 2 * (kPostRows + 3) * Wsp + (kPostRows + 1) * Wx + 64;
-  if (p.post_smem > 48 * 1024 &&
-      (e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
-    return e;
+  // 2 rows x 512 threads per CTA: measured best at c2/c3 among {1,2,4} x {256,512}
+  p.post_rows = 2;
+  p.post_threads = 512;
+  {
+    const int R = p.post_rows;
+    p.post_smem = (R + 3) * Wsp + (R + 1) * Wsp + (R + 1) * Wsp * 4 + (R + 1) * Wx * 4 +
+                  3 * (R + 1) * 64 * 4 + (R + 1) * Wsp * 2 + 2 * (R + 3) * Wsp + (R + 1) * Wx + 64;
+  }
+  if (p.post_smem > 48 * 1024) {
+    for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>})
+      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
+        return e;
+  }
   if (p.sd_smem > 48 * 1024) {
     switch (g.m_pool) {
       case 0: e = cudaFuncSetAttribute(sd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
