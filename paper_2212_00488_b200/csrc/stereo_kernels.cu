@@ -612,19 +612,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // CA = (lo_b - lo_a) + ((hi_b - hi_a) << 24).  12 bytes of prefix per two
 // disparities instead of 16, i.e. fewer shared-memory wavefronts per output.
 // The argmin key CA << 8 | d (CA < 2^40, d < 256) is then two 32-bit words
-// {lo << 8 | d, (lo >> 24) + hi}: two ALU operations, no 64-bit shifts; the u64
+// {lo << 8 | d, (lo >> 24) + hi}: two ALU operations, no 64-bit shifts; the
 // minimum of the keys is the paper's strict-< scan with ties to the smallest
 // d.
-constexpr int kYSplit = 24;
+constexpr int kYSplit = 24;  // = byte 3: the hi parts are extracted by byte permutes
 
+// The running minimum is kept as the IEEE double 2^52 + key (key < 2^48 is
+// exact and the map is monotone): one DSETP.MIN + two selects per candidate
+// instead of a 64-bit integer compare-and-select.  `hib` is the hi window sum
+// with the exponent bits 0x433 (2^52) already OR-ed in (hi < 2^16 + 2^8).
+constexpr uint32_t kYExp52 = 0x43300000u;
 template <bool DBG>
-__device__ __forceinline__ void ypass_take(uint64_t& best, uint32_t lo, uint32_t hi, int d,
+__device__ __forceinline__ void ypass_take(double& best, uint32_t lo, uint32_t hib, int d,
                                            uint64_t* cadbg, size_t dbg_idx, bool live) {
   const uint32_t klo = (lo << 8) | (uint32_t)d;
-  const uint32_t khi = (lo >> 24) + hi;
-  const uint64_t key = ((uint64_t)khi << 32) | klo;
-  best = min(best, key);
-  if (DBG && live) cadbg[dbg_idx] = key >> 8;
+  const uint32_t khi = (lo >> 24) + hib;
+  const double kd = __hiloint2double((int)khi, (int)klo);
+  if (kd < best) best = kd;  // never NaN: no fmin NaN fix-ups
+  if (DBG && live)
+    cadbg[dbg_idx] = ((((uint64_t)(khi - kYExp52)) << 32) | klo) >> 8;
 }
 
 // WTA over the window sums of d (and d+1 if TWO) for the thread's outputs
@@ -632,10 +638,10 @@ __device__ __forceinline__ void ypass_take(uint64_t& best, uint32_t lo, uint32_t
 // `z` is an opaque per-iteration zero: it keeps the optimiser from hoisting
 // four d-invariant addresses per output out of the d loop (register spills).
 template <int NR, bool TWO, bool DBG>
-__device__ __forceinline__ void ypass_wta(uint64_t (&best)[kYRPT], const uint32_t (&oab)[kYRPT],
+__device__ __forceinline__ void ypass_wta(double (&best)[kYRPT], const uint32_t (&oab)[kYRPT],
                                           const uint8_t* EloB, const uint8_t* EhiB, uint32_t z,
-                                          int d, uint64_t* cadbg, const YArgs& a, int yrow0,
-                                          int x) {
+                                          uint32_t e52, int d, uint64_t* cadbg, const YArgs& a,
+                                          int yrow0, int x) {
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const uint32_t v = oab[r] + z;
@@ -646,33 +652,34 @@ __device__ __forceinline__ void ypass_wta(uint64_t (&best)[kYRPT], const uint32_
                         *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
     const bool live = !DBG || (yrow0 + 16 * r < a.Hs && x < a.Ws);
     const size_t di = DBG ? ((size_t)d * a.Hs + yrow0 + 16 * r) * a.Ws + x : 0;
-    ypass_take<DBG>(best[r], lb.x - la.x, dh & 0xffffu, d, cadbg, di, live);
+    ypass_take<DBG>(best[r], lb.x - la.x, (dh & 0xffffu) | e52, d, cadbg, di, live);
     if (TWO)
-      ypass_take<DBG>(best[r], lb.y - la.y, dh >> 16, d + 1, cadbg,
+      ypass_take<DBG>(best[r], lb.y - la.y, (dh >> 16) + e52, d + 1, cadbg,
                       di + (DBG ? (size_t)a.Hs * a.Ws : 0), live);
   }
 }
 
 template <bool TWO, bool DBG>
-__device__ __forceinline__ void ypass_wta_n(int nr, uint64_t (&best)[kYRPT],
+__device__ __forceinline__ void ypass_wta_n(int nr, double (&best)[kYRPT],
                                             const uint32_t (&oab)[kYRPT], const uint8_t* EloB,
                                             const uint8_t* EhiB, int d, uint64_t* cadbg,
                                             const YArgs& a, int yrow0, int x) {
-  uint32_t z;
+  uint32_t z, e52;  // opaque: keeps the optimiser from re-associating the exponent bits
   asm volatile("mov.u32 %0, 0;" : "=r"(z));
+  asm volatile("mov.u32 %0, %1;" : "=r"(e52) : "n"(kYExp52));
   switch (nr) {  // warp-uniform (depends on the row segment only)
-    case 12: ypass_wta<12, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 11: ypass_wta<11, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 10: ypass_wta<10, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 9: ypass_wta<9, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 8: ypass_wta<8, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 7: ypass_wta<7, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 6: ypass_wta<6, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 5: ypass_wta<5, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 4: ypass_wta<4, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 3: ypass_wta<3, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 2: ypass_wta<2, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
-    case 1: ypass_wta<1, TWO, DBG>(best, oab, EloB, EhiB, z, d, cadbg, a, yrow0, x); break;
+    case 12: ypass_wta<12, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 11: ypass_wta<11, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 10: ypass_wta<10, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 9: ypass_wta<9, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 8: ypass_wta<8, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 7: ypass_wta<7, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 6: ypass_wta<6, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 5: ypass_wta<5, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 4: ypass_wta<4, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 3: ypass_wta<3, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 2: ypass_wta<2, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 1: ypass_wta<1, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
     default: break;
   }
 }
@@ -727,12 +734,12 @@ __global__ void __launch_bounds__(kYThreads, 2)
   // window byte offsets into Elo (Ehi: half of it), packed a | b << 16
   // (< 2^16: (TB+1)*16*8 <= 30848), and the running minimum keys
   uint32_t oab[kYRPT];
-  uint64_t best[kYRPT];
+  double best[kYRPT];
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r) {
     const int y = y0 + seg + 16 * r;
     oab[r] = 0u;
-    best[r] = ~0ull;
+    best[r] = __hiloint2double(0x7ff00000, 0);  // +inf
     if (r < nr && x < a.Ws) {
       const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
       const int M = (arm >> 16) & 255u, N = arm >> 24;
@@ -759,7 +766,7 @@ __global__ void __launch_bounds__(kYThreads, 2)
       const uint32_t v0 = t0[s * 16], v1 = t1[s * 16];
       a0 += v0 & kLoMask;
       a1 += v1 & kLoMask;
-      ah += (v0 >> kYSplit) | ((v1 >> (kYSplit - 16)) & 0xffff0000u);
+      ah += __byte_perm(v0, 0u, 0x4443u) + __byte_perm(v1, 0u, 0x4344u);  // v0.b3 | v1.b3 << 16
       l0[s] = a0; l1[s] = a1; lh[s] = ah;
     }
     // the warp's two segments: the upper half adds the lower half's totals
@@ -790,7 +797,7 @@ __global__ void __launch_bounds__(kYThreads, 2)
   }
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r)
-    if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(best[r] & 255u);
+    if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(__double2loint(best[r]) & 255);
 }
 
 #define YPASS_DISPATCH(S_, EXPR)                       \
