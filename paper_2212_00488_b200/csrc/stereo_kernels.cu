@@ -622,26 +622,21 @@ constexpr int kYSplit = 24;  // = byte 3: the hi parts are extracted by byte per
 // instead of a 64-bit integer compare-and-select.  `hib` is the hi window sum
 // with the exponent bits 0x433 (2^52) already OR-ed in (hi < 2^16 + 2^8).
 constexpr uint32_t kYExp52 = 0x43300000u;
-template <bool DBG>
-__device__ __forceinline__ void ypass_take(double& best, uint32_t lo, uint32_t hib, int d,
-                                           uint64_t* cadbg, size_t dbg_idx, bool live) {
+__device__ __forceinline__ void ypass_take(double& best, uint32_t lo, uint32_t hib, int d) {
   const uint32_t klo = (lo << 8) | (uint32_t)d;
   const uint32_t khi = (lo >> 24) + hib;
   const double kd = __hiloint2double((int)khi, (int)klo);
   if (kd < best) best = kd;  // never NaN: no fmin NaN fix-ups
-  if (DBG && live)
-    cadbg[dbg_idx] = ((((uint64_t)(khi - kYExp52)) << 32) | klo) >> 8;
 }
 
 // WTA over the window sums of d (and d+1 if TWO) for the thread's outputs
 // r < NR (NR warp-uniform: straight-line code the scheduler can interleave).
 // `z` is an opaque per-iteration zero: it keeps the optimiser from hoisting
 // four d-invariant addresses per output out of the d loop (register spills).
-template <int NR, bool TWO, bool DBG>
+template <int NR, bool TWO>
 __device__ __forceinline__ void ypass_wta(double (&best)[kYRPT], const uint32_t (&oab)[kYRPT],
                                           const uint8_t* EloB, const uint8_t* EhiB, uint32_t z,
-                                          uint32_t e52, int d, uint64_t* cadbg, const YArgs& a,
-                                          int yrow0, int x) {
+                                          uint32_t e52, int d) {
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const uint32_t v = oab[r] + z;
@@ -650,37 +645,52 @@ __device__ __forceinline__ void ypass_wta(double (&best)[kYRPT], const uint32_t 
     const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
     const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
                         *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
-    const bool live = !DBG || (yrow0 + 16 * r < a.Hs && x < a.Ws);
-    const size_t di = DBG ? ((size_t)d * a.Hs + yrow0 + 16 * r) * a.Ws + x : 0;
-    ypass_take<DBG>(best[r], lb.x - la.x, (dh & 0xffffu) | e52, d, cadbg, di, live);
-    if (TWO)
-      ypass_take<DBG>(best[r], lb.y - la.y, (dh >> 16) + e52, d + 1, cadbg,
-                      di + (DBG ? (size_t)a.Hs * a.Ws : 0), live);
+    ypass_take(best[r], lb.x - la.x, (dh & 0xffffu) | e52, d);
+    if (TWO) ypass_take(best[r], lb.y - la.y, (dh >> 16) + e52, d + 1);
   }
 }
 
-template <bool TWO, bool DBG>
+template <bool TWO>
 __device__ __forceinline__ void ypass_wta_n(int nr, double (&best)[kYRPT],
                                             const uint32_t (&oab)[kYRPT], const uint8_t* EloB,
-                                            const uint8_t* EhiB, int d, uint64_t* cadbg,
-                                            const YArgs& a, int yrow0, int x) {
+                                            const uint8_t* EhiB, int d) {
   uint32_t z, e52;  // opaque: keeps the optimiser from re-associating the exponent bits
   asm volatile("mov.u32 %0, 0;" : "=r"(z));
   asm volatile("mov.u32 %0, %1;" : "=r"(e52) : "n"(kYExp52));
   switch (nr) {  // warp-uniform (depends on the row segment only)
-    case 12: ypass_wta<12, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 11: ypass_wta<11, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 10: ypass_wta<10, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 9: ypass_wta<9, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 8: ypass_wta<8, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 7: ypass_wta<7, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 6: ypass_wta<6, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 5: ypass_wta<5, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 4: ypass_wta<4, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 3: ypass_wta<3, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 2: ypass_wta<2, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
-    case 1: ypass_wta<1, TWO, DBG>(best, oab, EloB, EhiB, z, e52, d, cadbg, a, yrow0, x); break;
+    case 12: ypass_wta<12, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 11: ypass_wta<11, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 10: ypass_wta<10, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 9: ypass_wta<9, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 8: ypass_wta<8, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 7: ypass_wta<7, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 6: ypass_wta<6, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 5: ypass_wta<5, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 4: ypass_wta<4, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 3: ypass_wta<3, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 2: ypass_wta<2, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
+    case 1: ypass_wta<1, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
     default: break;
+  }
+}
+
+// Debug volume (STEREO_DEBUG_CA): the exact window sums of d (and d+1) of the
+// thread's own rows, from the same prefix rows the WTA read.  A plain loop
+// (debug builds of the kernel only).
+__device__ __noinline__ void ypass_debug_store(const uint32_t* oab, int nr, const uint8_t* EloB,
+                                               const uint8_t* EhiB, int d, bool two,
+                                               uint64_t* cadbg, int Hs, int Ws, int yrow0,
+                                               int x) {
+  if (x >= Ws) return;
+  for (int r = 0; r < nr; ++r) {
+    const uint32_t ia = oab[r] & 0xffffu, ib = oab[r] >> 16;
+    const uint2 la = *reinterpret_cast<const uint2*>(EloB + ia);
+    const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
+    const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
+                        *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
+    const size_t o = ((size_t)d * Hs + yrow0 + 16 * r) * Ws + x;
+    cadbg[o] = (uint64_t)(lb.x - la.x) + ((uint64_t)(dh & 0xffffu) << kYSplit);
+    if (two) cadbg[o + (size_t)Hs * Ws] = (uint64_t)(lb.y - la.y) + ((uint64_t)(dh >> 16) << kYSplit);
   }
 }
 
@@ -791,9 +801,10 @@ __global__ void __launch_bounds__(kYThreads, 2)
     }
     __syncthreads();  // (2) column prefixes complete
     if (d + 1 < Ds)
-      ypass_wta_n<true, DBG>(nrw, best, oab, EloB, EhiB, d, cadbg, a, y0 + seg, x);
+      ypass_wta_n<true>(nrw, best, oab, EloB, EhiB, d);
     else
-      ypass_wta_n<false, DBG>(nrw, best, oab, EloB, EhiB, d, cadbg, a, y0 + seg, x);
+      ypass_wta_n<false>(nrw, best, oab, EloB, EhiB, d);
+    if (DBG) ypass_debug_store(oab, nr, EloB, EhiB, d, d + 1 < Ds, cadbg, a.Hs, a.Ws, y0 + seg, x);
   }
 #pragma unroll
   for (int r = 0; r < kYRPT; ++r)
@@ -1322,7 +1333,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   const int nb0 = (g.Hs + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
   p.ypass_nb = 0;
-  for (int nb = nb0; nb <= g.Hs && nb <= 4 * nb0 + 8; ++nb) {
+  for (int nb = nb0; nb <= g.Hs; ++nb) {
     const int B = (g.Hs + nb - 1) / nb;
     const int SEG = ypass_seg_for(B + 2 * g.w_y);
     if (!SEG) continue;

@@ -186,6 +186,54 @@ def test_ca_volume_bit_exact_and_tolerance_vs_double():
         assert rel.max() <= 1e-5  # north_star tolerance
 
 
+def _ca_volumes(L, R, D, kw):
+    H, W = L.shape
+    st = abi.Stereo(W, H, D, **kw)
+    st.set_debug(abi.DEBUG_CA, True)
+    _run_gpu(L, R, D, st=st, **kw)
+    caL, caR, DL, DR = (st.download(b) for b in (abi.BUF_CA_L, abi.BUF_CA_R, abi.BUF_DL, abi.BUF_DR))
+    st.close()
+    return caL, caR, DL, DR
+
+
+@pytest.mark.parametrize("case", [
+    # several 16-column strips and row bands, odd D_s (the last disparity pair
+    # has one member), ragged last strip / band
+    dict(W=301, H=263, D=45, kw=dict(k_scale=1), img="scene"),
+    # the largest vertical window the y tile allows (2*112+1 = 225 rows) with
+    # x sums at their maximum (every term BORDER for x < d, or AD = 255):
+    # exercises the exact lo/hi split of the column prefix at its limits
+    dict(W=60, H=300, D=40, kw=dict(k_scale=1, w_y=112), img="flat"),
+    dict(W=60, H=300, D=12, kw=dict(k_scale=1, w_y=112, w_x=60), img="extreme"),
+])
+def test_ca_volume_split_prefix_extremes(case):
+    W, H, D, kw = case["W"], case["H"], case["D"], case["kw"]
+    if case["img"] == "scene":
+        L, R, _ = synth.scene(W, H, D, seed=9)
+    elif case["img"] == "flat":
+        L = np.full((H, W), 90, np.uint8)
+        R = L.copy()
+    else:  # maximal AD everywhere, flat (arms at their caps)
+        L = np.zeros((H, W), np.uint8)
+        R = np.full((H, W), 255, np.uint8)
+    caL, caR, DL, DR = _ca_volumes(L, R, D, kw)
+    ref = oracle.pipeline(L, R, D, _oracle_params(kw), "fixed", stages=("caL", "caR", "DL", "DR"))
+    for a, b in ((caL, ref["caL"]), (caR, ref["caR"]), (DL, ref["DL"]), (DR, ref["DR"])):
+        assert np.array_equal(a, b)
+    if case["img"] != "scene":  # the windows really reach the split's limits
+        f = oracle.fixed_bits(kw.get("w_x", 21))
+        assert int(caL.max()) >= 200 * (2 ** 24) and int(caL.max()) < 2 ** 41 and f >= 22
+
+
+@pytest.mark.parametrize("W,H,D", [
+    (1444, 960, 380),   # NEXT-2 (i): Vintage-shaped, D_s = 190
+    (1482, 994, 128),   # NEXT-2 (ii): Pipes-shaped
+])
+def test_next2_workloads_bit_exact(W, H, D):
+    L, R, _ = synth.scene(W, H, D, seed=3)
+    _compare(L, R, D, dict(), volumes=False)
+
+
 def test_disparity_maps_vs_double_definition():
     """<= 0.01% of D^L/D^R pixels may differ from the double-mode oracle, and
     only where the two candidates' double costs tie within 1e-5 (north_star)."""
