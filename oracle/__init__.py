@@ -47,7 +47,12 @@ class Params(C.Structure):
         ("w_x", C.c_int32), ("w_y", C.c_int32), ("delta", C.c_int32),
         ("k_scale", C.c_int32), ("m_pool", C.c_int32),
         ("census_dx", C.c_int32 * 6), ("census_dy", C.c_int32 * 6),
+        ("w_x_r", C.c_int32), ("fill_mode", C.c_int32),
     ]
+
+
+# §III.E non-GCP filling modes (oracle/stereo_oracle.h OR_FILL_*)
+FILL_MODES = {"bilateral": 0, "nearest": 1, "smaller": 2, "eq11_literal": 3}
 
 
 # S:92 default pattern (reading R8): (0,-2)(-1,-1)(+1,-1)(-1,+1)(+1,+1)(0,+2)
@@ -55,11 +60,14 @@ DEFAULT_CENSUS = ((0, -2), (-1, -1), (1, -1), (-1, 1), (1, 1), (0, 2))
 
 
 def params(lambda_ad=0.3, lambda_mc=2.3, t_fill=3, w_x=21, w_y=31, delta=20, k_scale=2,
-           m_pool=1, census=DEFAULT_CENSUS) -> Params:
-    """P:609 (lambda_AD, lambda_MC, T), P:621-622 (W_x, W_y), S:90 (delta), P:155 (K)."""
+           m_pool=1, census=DEFAULT_CENSUS, w_x_r=-1, fill_mode=0) -> Params:
+    """P:609 (lambda_AD, lambda_MC, T), P:621-622 (W_x, W_y), S:90 (delta), P:155 (K);
+    w_x_r: right-base x cap (-1 = w_x); fill_mode: FILL_MODES value or name."""
     p = Params()
     p.lambda_ad, p.lambda_mc, p.t_fill = lambda_ad, lambda_mc, t_fill
     p.w_x, p.w_y, p.delta, p.k_scale, p.m_pool = w_x, w_y, delta, k_scale, m_pool
+    p.w_x_r = w_x_r
+    p.fill_mode = FILL_MODES[fill_mode] if isinstance(fill_mode, str) else fill_mode
     for i, (dx, dy) in enumerate(census):
         p.census_dx[i], p.census_dy[i] = dx, dy
     return p
@@ -110,7 +118,8 @@ def lib():
                 "or_wta_u64": (None, [u64p, C.c_int, C.c_int, C.c_int, u8p]),
                 "or_cross_check": (None, [u8p, u8p, C.c_int, C.c_int, u8p]),
                 "or_median3x3": (None, [u8p, C.c_int, C.c_int, u8p]),
-                "or_fill_bilateral": (None, [u8p, u8p, C.c_int, C.c_int, C.c_int, f32p]),
+                "or_fill_bilateral": (None, [u8p, u8p, C.c_int, C.c_int, C.c_int, C.c_int, f32p]),
+                "or_rgb_to_gray": (None, [u8p, C.c_int, C.c_int, u8p]),
                 "or_scale_up": (None, [f32p, C.c_int, C.c_int, u8p, C.c_int, C.c_int, C.c_int,
                                        C.c_int, f32p]),
                 "or_pipeline": (C.c_int, [u8p, u8p, C.c_int, C.c_int, C.c_int, C.POINTER(Params),
@@ -255,11 +264,21 @@ def median3x3(m):
     return out
 
 
-def fill_bilateral(med, Limg, T=3):
+def fill_bilateral(med, Limg, T=3, mode=0):
     med, Limg = _u8(med), _u8(Limg)
     H, W = med.shape
     out = np.zeros((H, W), np.float32)
-    lib().or_fill_bilateral(med, Limg, W, H, T, out)
+    mode = FILL_MODES[mode] if isinstance(mode, str) else mode
+    lib().or_fill_bilateral(med, Limg, W, H, T, mode, out)
+    return out
+
+
+def rgb_to_gray(rgb):
+    """§III item 1, BT.601 reading: rgb u8 [H][W][3] -> u8 [H][W]."""
+    rgb = _u8(rgb)
+    H, W, _ = rgb.shape
+    out = np.zeros((H, W), np.uint8)
+    lib().or_rgb_to_gray(rgb, W, H, out)
     return out
 
 

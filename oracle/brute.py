@@ -127,7 +127,10 @@ def median3x3(mm):
     return out
 
 
-def fill(med, Limg, T):
+def fill(med, Limg, T, mode="bilateral"):
+    """§III.E: mode 'bilateral' (Eq. 11 read as interpolation),
+    'nearest' / 'smaller' (Fig. 6 (a)/(b), P:264-274), 'eq11_literal' (P:292
+    as printed)."""
     H, W = len(med), len(med[0])
     out = [[0.0] * W for _ in range(H)]
     valid_rows = [[x for x in range(W) if med[y][x] != INVALID] for y in range(H)]
@@ -153,14 +156,39 @@ def fill(med, Limg, T):
             if left and right:
                 i, j = x - left[-1], right[0] - x
                 Dl, Dr = med[y][left[-1]], med[y][right[0]]
-                if abs(Dl - Dr) <= T:
-                    # D_l + i*(D_r - D_l)/(i+j), rounded once to binary32
-                    out[y][x] = float(np.float32(float(Fraction(Dl) + i * Fraction(Dr - Dl, i + j))))
+                if mode == "nearest":
+                    out[y][x] = float(Dl if i <= j else Dr)   # equal distance -> left
+                elif mode == "smaller":
+                    out[y][x] = float(min(Dl, Dr))
+                elif abs(Dl - Dr) <= T:
+                    if mode == "eq11_literal":  # D_l + i*(D_l - D_r)/(i+j), rounded once
+                        v = Fraction(Dl) + i * Fraction(Dl - Dr, i + j)
+                    else:                       # D_l + i*(D_r - D_l)/(i+j), rounded once
+                        v = Fraction(Dl) + i * Fraction(Dr - Dl, i + j)
+                    out[y][x] = _f32_of_fraction(v)
                 else:
                     c = Limg[y][x]
                     out[y][x] = float(Dl if abs(Limg[y][x - i] - c) <= abs(Limg[y][x + j] - c) else Dr)
             else:
                 out[y][x] = float(med[y][left[-1]] if left else med[y][right[0]])
+    return out
+
+
+def _f32_of_fraction(v: Fraction) -> float:
+    """Round an exact rational once to binary32 (via the correctly-rounded
+    double: |numerator| < 2^24, denominator < 2^12, so no double rounding)."""
+    return float(np.float32(v.numerator / v.denominator))
+
+
+def rgb_to_gray(rgb):
+    """BT.601 luma rounded half up (reading R31), via exact rationals."""
+    out = []
+    for row in rgb:
+        o = []
+        for r, g, b in row:
+            v = Fraction(299, 1000) * r + Fraction(587, 1000) * g + Fraction(114, 1000) * b
+            o.append(math.floor(v + Fraction(1, 2)))
+        out.append(o)
     return out
 
 

@@ -322,7 +322,7 @@ void or_median3x3(const uint8_t* in, int W, int H, uint8_t* out) {
  *      one); if none, the first valid pixel of the nearest such row below; if
  *      the whole map is invalid, 0 (reading R25b). */
 void or_fill_bilateral(const uint8_t* med, const uint8_t* Limg, int W, int H, int T,
-                       float* out) {
+                       int mode, float* out) {
   for (int y = 0; y < H; ++y) {
     const uint8_t* row = med + (size_t)y * W;
     const uint8_t* lrow = Limg + (size_t)y * W;
@@ -338,8 +338,16 @@ void or_fill_bilateral(const uint8_t* med, const uint8_t* Limg, int W, int H, in
       int hl = x - i >= 0, hr = x + j < W;
       if (hl && hr) {
         int Dl = row[x - i], Dr = row[x + j];
-        if (iabs(Dl - Dr) <= T) {
-          orow[x] = (float)(Dl * j + Dr * i) / (float)(i + j);
+        if (mode == OR_FILL_NEAREST) {          /* Fig. 6(a); tie -> left */
+          orow[x] = (float)(i <= j ? Dl : Dr);
+        } else if (mode == OR_FILL_SMALLER) {   /* Fig. 6(b) */
+          orow[x] = (float)(Dl < Dr ? Dl : Dr);
+        } else if (iabs(Dl - Dr) <= T) {
+          if (mode == OR_FILL_EQ11_LITERAL)     /* D(x-i) + i (D(x-i) - D(x+j)) / (i+j), P:292,
+                                                   as one exact rational rounded once */
+            orow[x] = (float)(Dl * (i + j) + i * (Dl - Dr)) / (float)(i + j);
+          else
+            orow[x] = (float)(Dl * j + Dr * i) / (float)(i + j);
         } else {
           int c = lrow[x];
           orow[x] = (iabs(lrow[x - i] - c) <= iabs(lrow[x + j] - c)) ? (float)Dl : (float)Dr;
@@ -365,6 +373,13 @@ void or_fill_bilateral(const uint8_t* med, const uint8_t* Limg, int W, int H, in
       for (int x = 0; x < W; ++x)
         if (med[(size_t)yy * W + x] != OR_INVALID) { v = (float)med[(size_t)yy * W + x]; found = 1; break; }
     for (int x = 0; x < W; ++x) out[(size_t)y * W + x] = v;
+  }
+}
+
+void or_rgb_to_gray(const uint8_t* rgb, int W, int H, uint8_t* gray) {
+  for (size_t k = 0; k < (size_t)W * H; ++k) {
+    const int r = rgb[3 * k], g = rgb[3 * k + 1], b = rgb[3 * k + 2];
+    gray[k] = (uint8_t)((299 * r + 587 * g + 114 * b + 500) / 1000);
   }
 }
 
@@ -427,7 +442,8 @@ static int validate(int W, int H, int D, const or_params* p) {
   if (p->k_scale > 2 || p->m_pool < 0) return -1;
   if (W / p->k_scale < 1 || H / p->k_scale < 1) return -1;
   if (or_scaled_max_disparity(D, p->k_scale) > 255) return -1;
-  if (p->w_x > 254 || p->w_y > 254) return -1;
+  if (p->w_x > 254 || p->w_y > 254 || p->w_x_r > 254) return -1;
+  if (p->fill_mode < OR_FILL_BILATERAL || p->fill_mode > OR_FILL_EQ11_LITERAL) return -1;
   return 0;
 }
 
@@ -454,11 +470,12 @@ int or_pipeline(const uint8_t* Lorg, const uint8_t* Rorg, int W, int H, int D,
   or_census(Rs, Ws, Hs, p->census_dx, p->census_dy, cR);
   or_arms_x(Ls, Ws, Hs, p->delta, p->w_x, aL, aL + n);
   or_arms_y(Ls, Ws, Hs, p->delta, p->w_y, aL + 2 * n, aL + 3 * n);
-  or_arms_x(Rs, Ws, Hs, p->delta, p->w_x, aR, aR + n);
+  const int wxr = p->w_x_r < 0 ? p->w_x : p->w_x_r;  /* P:613-619 */
+  or_arms_x(Rs, Ws, Hs, p->delta, wxr, aR, aR + n);
   or_arms_y(Rs, Ws, Hs, p->delta, p->w_y, aR + 2 * n, aR + 3 * n);
 
   if (mode == OR_MODE_FIXED) {
-    const int f = or_fixed_bits(p->w_x);
+    const int f = or_fixed_bits(p->w_x > wxr ? p->w_x : wxr);
     uint32_t qad[256], qmc[7];
     or_fixed_tables(p->lambda_ad, p->lambda_mc, f, qad, qmc);
     const uint32_t border = (uint32_t)1 << (f + 1);
@@ -522,7 +539,7 @@ int or_pipeline(const uint8_t* Lorg, const uint8_t* Rorg, int W, int H, int D,
   or_cross_check(DL, DR, Ws, Hs, msk);
   or_median3x3(msk, Ws, Hs, med);
   float* fill = (float*)malloc(n * sizeof(float));
-  or_fill_bilateral(med, Ls, Ws, Hs, p->t_fill, fill);
+  or_fill_bilateral(med, Ls, Ws, Hs, p->t_fill, p->fill_mode, fill);
   if (o->out) {
     if (K == 1) memcpy(o->out, fill, n * sizeof(float));
     else or_scale_up(fill, Ws, Hs, Lorg, W, H, K, p->t_fill, o->out);

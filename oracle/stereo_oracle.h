@@ -39,7 +39,18 @@ typedef struct {
   int32_t k_scale;      /* K = 2; 1 = no scaling */
   int32_t m_pool;       /* m = 1 */
   int32_t census_dx[6], census_dy[6];  /* mini-census pattern */
+  int32_t w_x_r;        /* x cap of the RIGHT-base arms, < 0 = w_x: "(W_x, W_y) can be
+                           changed when calculating D^L and D^R", W_y common */
+  int32_t fill_mode;    /* OR_FILL_*: non-GCP filling, §III.E */
 } or_params;
+
+/* non-GCP filling (§III.E): the bilateral estimation (Eq. 11 read
+ * as the interpolation, reading E6), the two baselines of Fig. 6
+ * and Eq. 11 exactly as printed (NEXT-3) */
+#define OR_FILL_BILATERAL 0
+#define OR_FILL_NEAREST 1
+#define OR_FILL_SMALLER 2
+#define OR_FILL_EQ11_LITERAL 3
 
 typedef struct {          /* every pointer may be NULL (= not requested) */
   uint8_t *Ls, *Rs;       /* scaled images [Hs][Ws] */
@@ -104,7 +115,11 @@ void or_cross_check(const uint8_t* DL, const uint8_t* DR, int W, int H, uint8_t*
 /* Step7 */
 void or_median3x3(const uint8_t* in, int W, int H, uint8_t* out);
 void or_fill_bilateral(const uint8_t* med, const uint8_t* Limg, int W, int H, int T,
-                       float* out);
+                       int mode, float* out);
+/* §III list item 1 "the two input images are gray-scaled"; formula
+ * unstated -> BT.601 luma, round half up (reading R31):
+ * gray = floor((299 R + 587 G + 114 B + 500) / 1000); rgb is [H][W][3] */
+void or_rgb_to_gray(const uint8_t* rgb, int W, int H, uint8_t* gray);
 /* Step8 */
 void or_scale_up(const float* v, int Ws, int Hs, const uint8_t* Lorg, int W, int H,
                  int K, int T, float* out);

@@ -22,10 +22,13 @@ def _rand_params(rng):
         pat = tuple(cand[i] for i in idx)
     return dict(delta=int(rng.choice([13, 20, int(rng.integers(1, 60))])),
                 w_x=int(rng.integers(0, 6)), w_y=int(rng.integers(0, 6)),
-                t_fill=int(rng.integers(0, 5)), census=pat)
+                t_fill=int(rng.integers(0, 5)), census=pat,
+                # NEXT-3 variants: right-base x cap, fill mode (§III.E)
+                w_x_r=int(rng.choice([-1, int(rng.integers(0, 6))])),
+                fill_mode=str(rng.choice(list(oracle.FILL_MODES))))
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(24))
 def test_stages_vs_brute(seed):
     rng = np.random.default_rng(seed)
     K = int(rng.choice([1, 2]))
@@ -48,7 +51,8 @@ def test_stages_vs_brute(seed):
     cL, cR = brute.census(Ls, kw["census"]), brute.census(Rs, kw["census"])
     assert r["cenL"].tolist() == cL and r["cenR"].tolist() == cR
     aL = brute.arms(Ls, kw["delta"], kw["w_x"], kw["w_y"])
-    aR = brute.arms(Rs, kw["delta"], kw["w_x"], kw["w_y"])
+    wxr = kw["w_x"] if kw["w_x_r"] < 0 else kw["w_x_r"]
+    aR = brute.arms(Rs, kw["delta"], wxr, kw["w_y"])
     assert [a.tolist() for a in r["armL"]] == list(aL)
     assert [a.tolist() for a in r["armR"]] == list(aR)
 
@@ -73,7 +77,7 @@ def test_stages_vs_brute(seed):
     assert r["masked"].tolist() == mm
     med = brute.median3x3(mm)
     assert r["median"].tolist() == med
-    fl = brute.fill(med, Ls, kw["t_fill"])
+    fl = brute.fill(med, Ls, kw["t_fill"], kw["fill_mode"])
     assert np.array_equal(r["fill"], np.array(fl, np.float32))
     out = brute.scale_up(fl, Lorg.tolist(), K, kw["t_fill"])
     assert np.array_equal(r["out"], np.array(out, np.float32))
@@ -103,3 +107,26 @@ def test_fixed_mode_equals_quantised_sums(seed):
                for x in range(W)] for y in range(H)]
         assert r["caL"][d].tolist() == [[int(v) for v in row] for row in brute.aggregate_cross(QL, *aL)]
         assert r["caR"][d].tolist() == [[int(v) for v in row] for row in brute.aggregate_cross(QR, *aR)]
+
+
+@pytest.mark.parametrize("mode", list(oracle.FILL_MODES))
+@pytest.mark.parametrize("seed", range(4))
+def test_fill_modes_vs_brute(mode, seed):
+    """Every §III.E filling mode on random sparse maps (many non-GCP runs,
+    rows without any valid pixel)."""
+    rng = np.random.default_rng(900 + seed)
+    H, W = 7, 17
+    med = rng.integers(0, 40, (H, W)).astype(np.uint8)
+    med[rng.random((H, W)) < 0.6] = 255
+    med[3] = 255
+    Limg = rng.integers(0, 256, (H, W)).astype(np.uint8)
+    T = int(rng.integers(0, 12))
+    got = oracle.fill_bilateral(med, Limg, T, mode)
+    ref = np.array(brute.fill(med.tolist(), Limg.tolist(), T, mode), np.float32)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_rgb_to_gray_vs_brute():
+    rng = np.random.default_rng(7)
+    rgb = rng.integers(0, 256, (9, 13, 3)).astype(np.uint8)
+    assert oracle.rgb_to_gray(rgb).tolist() == brute.rgb_to_gray(rgb.tolist())

@@ -364,3 +364,52 @@ def test_scale_up_sharp_edge():
 def test_mde_formula(golden):
     g = golden["mde_per_s"]
     assert round(g["W"] * g["H"] * g["D"] * g["fps"] / 1e6) == g["expected_formula"]
+
+
+def test_fill_variant_examples(golden):
+    """NEXT-3 fill variants (§III.E, Fig. 6 and the printed Eq. 11)."""
+    g = golden["fill_variants"]
+    for key in ("eq11_literal_spec_example", "eq11_literal_thirds"):
+        e = g[key]
+        W = e["i"] + e["j"] + 1
+        row = np.full((1, W), 255, np.uint8)
+        row[0, 0], row[0, W - 1] = e["Dl"], e["Dr"]
+        got = oracle.fill_bilateral(row, np.zeros((1, W), np.uint8), e["T"], "eq11_literal")[0, e["i"]]
+        want = e["expected"] if "expected" in e else np.float32(e["expected_fraction"][0] / e["expected_fraction"][1])
+        assert got == want
+    e = g["nearest"]
+    W = e["i"] + e["j"] + 1
+    row = np.full((1, W), 255, np.uint8)
+    row[0, 0], row[0, W - 1] = e["Dl"], e["Dr"]
+    out = oracle.fill_bilateral(row, np.zeros((1, W), np.uint8), 3, "nearest")
+    assert out[0, e["i"]] == e["expected"]
+    assert out[0, W - 2] == e["Dr"]                     # the closer side is the right one
+    row2 = np.array([[e["Dl"], 255, 255, 255, e["Dr"]]], np.uint8)
+    assert oracle.fill_bilateral(row2, np.zeros((1, 5), np.uint8), 3, "nearest")[0, 2] == e["Dl"]
+    e = g["smaller"]
+    W = e["i"] + e["j"] + 1
+    row = np.full((1, W), 255, np.uint8)
+    row[0, 0], row[0, W - 1] = e["Dl"], e["Dr"]
+    out = oracle.fill_bilateral(row, np.zeros((1, W), np.uint8), 100, "smaller")
+    assert (out[0, 1:W - 1] == e["expected"]).all()
+    # the baselines ignore T and brightness; the literal Eq. 11 keeps the edge rule
+    row = np.array([[10, 255, 30]], np.uint8)
+    Lb = np.array([[90, 52, 50]], np.uint8)
+    assert oracle.fill_bilateral(row, Lb, 3, "eq11_literal")[0, 1] == 30.0
+    assert oracle.fill_bilateral(row, Lb, 3, "nearest")[0, 1] == 10.0
+
+
+def test_rgb_to_gray_examples(golden):
+    for (r, g, b), want in golden["rgb_to_gray"]["examples"]:
+        rgb = np.array([[[r, g, b]]], np.uint8)
+        assert oracle.rgb_to_gray(rgb)[0, 0] == want
+
+
+def test_right_base_arm_cap():
+    """w_x_r caps only the right-base x arms; W_y stays common."""
+    L = np.full((6, 40), 77, np.uint8)
+    r = oracle.pipeline(L, L, 4, oracle.params(k_scale=1, w_x=5, w_x_r=2), "fixed",
+                        stages=("armL", "armR"))
+    assert r["armL"][0].max() == 5 and r["armL"][1].max() == 5
+    assert r["armR"][0].max() == 2 and r["armR"][1].max() == 2
+    assert np.array_equal(r["armL"][2:], r["armR"][2:])
