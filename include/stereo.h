@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define STEREO_ABI_VERSION 1u
+#define STEREO_ABI_VERSION 2u
 
 enum {
   STEREO_OK = 0,
@@ -66,7 +66,22 @@ typedef struct {
   int32_t m_pool;        /* mean-pool radius m of Eq. 2; 0..3 */
   int8_t census_dx[6];   /* the six mini-census offsets, |dx|,|dy| <= 2, */
   int8_t census_dy[6];   /* distinct and non-zero; bit i <-> offset i */
+  /* ABI 2: the NEXT-3 method variants */
+  int32_t w_x_r;         /* x arm cap of the RIGHT-base map D^R: "(W_x, W_y) can be
+                            changed when calculating D^L and D^R", W_y common
+                            (P:613-619); -1 = w_x (default); else 0..254 */
+  int32_t fill_mode;     /* non-GCP filling, §III.E: STEREO_FILL_* (default 0) */
 } stereo_params;
+
+/* Non-GCP filling modes (§III.E). */
+enum {
+  STEREO_FILL_BILATERAL = 0,    /* the paper's method, steps 1-3, Eq. 11
+                                   read as the interpolation (reading E6) */
+  STEREO_FILL_NEAREST = 1,      /* Fig. 6(a): the closer GCP's disparity (tie: left) */
+  STEREO_FILL_SMALLER = 2,      /* Fig. 6(b): the smaller of the two disparities */
+  STEREO_FILL_EQ11_LITERAL = 3  /* steps 1-3 with Eq. 11 exactly as printed:
+                                   D(x-i) + i (D(x-i) - D(x+j)) / (i+j) */
+};
 
 /* Derived sizes and resources of a handle (filled by stereo_get_info). */
 typedef struct {
@@ -92,8 +107,9 @@ void stereo_default_params(stereo_params* p);
  * t_fill >= 0, w_x >= 0, w_y >= 0, k_scale >= 1, D >= 1, W >= 1, H >= 1,
  * W/K >= 1, H/K >= 1, six distinct non-zero census offsets -> STEREO_EINVAL.
  * STEREO_EUNSUPPORTED for K not in {1,2}, ceil(D/K) > 255 (u8 maps use 255 as
- * INVALID), w_x > 254 (u8 arms), w_y > 112 (the y-aggregation tile holds
- * B + 2*w_y <= 240 rows), census offsets beyond +-2, m_pool > 3.
+ * INVALID), w_x or w_x_r > 254 (u8 arms), w_y > 112 (the y-aggregation tile
+ * holds B + 2*w_y <= 240 rows), census offsets beyond +-2, m_pool > 3.
+ * STEREO_EINVAL also for w_x_r < -1 and fill_mode outside STEREO_FILL_*.
  * Allocates every device buffer (dominant: two u32 CA_x volumes of
  * Ds*Hs*Ws*4 bytes each), builds the fixed-point cost tables on the host in
  * double precision and uploads them.  No kernel runs.  On success *out owns
@@ -184,6 +200,20 @@ enum {
 };
 int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,
                      float* disp_out, void* stream);
+
+/* Gray front end, §III list item 1 ("the two input images are
+ * gray-scaled"; the formula is unstated -> BT.601 luma rounded half up,
+ * reading R31): gray = floor((299 R + 587 G + 114 B + 500) / 1000).
+ * rgb: DEVICE u8 [H][W][3] interleaved; gray: DEVICE u8 [H][W]; enqueued on
+ * `stream` (cudaStream_t, NULL = legacy default).  STEREO_EINVAL for NULL
+ * pointers or W, H < 1. */
+int stereo_rgb_to_gray(const uint8_t* rgb, uint8_t* gray, int W, int H, void* stream);
+
+/* stereo_compute for colour inputs: L_rgb, R_rgb DEVICE u8 [H][W][3]; the
+ * gray conversion runs into handle-owned buffers, then the normal pipeline.
+ * Same ownership / error rules as stereo_compute. */
+int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb,
+                       float* disp_out, void* stream);
 
 /* Row-band support.  A band of a frame is computed by running
  * the normal pipeline on a sub-image whose halo rows cover the dependency cone

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("STEREO_B200_LIB", os.path.join(_HERE, "lib", "libstereo_b200.so"))
 
-STEREO_ABI_VERSION = 1
+STEREO_ABI_VERSION = 2
 STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, -1, -2, -3, -4
 
 (BUF_PIX_L, BUF_PIX_R, BUF_ARM_L, BUF_ARM_R, BUF_CAX_L, BUF_CAX_R, BUF_CA_L, BUF_CA_R,
@@ -29,6 +29,9 @@ STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, 
 STAGE_NAMES = ("SD", "PREP", "XPASS", "YPASS", "POST")
 STAGE_COUNT = 5
 DEBUG_CA = 1
+# non-GCP filling modes (include/stereo.h STEREO_FILL_*, §III.E)
+FILL_BILATERAL, FILL_NEAREST, FILL_SMALLER, FILL_EQ11_LITERAL = range(4)
+FILL_MODES = {"bilateral": 0, "nearest": 1, "smaller": 2, "eq11_literal": 3}
 
 # every symbol include/stereo.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -36,6 +39,7 @@ EXPORTS = (
     "stereo_compute_host", "stereo_destroy", "stereo_last_error", "stereo_get_info",
     "stereo_get_tables", "stereo_debug_download", "stereo_debug_upload", "stereo_set_debug",
     "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms", "stereo_patch_rows",
+    "stereo_rgb_to_gray", "stereo_compute_rgb",
 )
 
 
@@ -55,6 +59,7 @@ class Params(C.Structure):
         ("t_fill", C.c_int32), ("w_x", C.c_int32), ("w_y", C.c_int32), ("delta", C.c_int32),
         ("k_scale", C.c_int32), ("m_pool", C.c_int32),
         ("census_dx", C.c_int8 * 6), ("census_dy", C.c_int8 * 6),
+        ("w_x_r", C.c_int32), ("fill_mode", C.c_int32),
     ]
 
 
@@ -105,6 +110,8 @@ def lib():
             "stereo_set_timing": (i32, [vp, i32]),
             "stereo_stage_times_ms": (i32, [vp, vp, C.POINTER(C.c_int)]),
             "stereo_patch_rows": (i32, [vp, vp, vp, i32, vp, vp, vp]),
+            "stereo_rgb_to_gray": (i32, [vp, vp, i32, i32, vp]),
+            "stereo_compute_rgb": (i32, [vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -122,6 +129,8 @@ def default_params(**overrides) -> Params:
     p = Params()
     lib().stereo_default_params(C.byref(p))
     census = overrides.pop("census", None)
+    if isinstance(overrides.get("fill_mode"), str):
+        overrides["fill_mode"] = FILL_MODES[overrides["fill_mode"]]
     for k, v in overrides.items():
         setattr(p, k, v)
     if census is not None:
@@ -189,6 +198,12 @@ class Stereo:
     def compute(self, L, R, out, stream=None):
         """L, R: CUDA u8 [H][W]; out: CUDA f32 [H][W]. Enqueued, not synchronised."""
         _check(lib().stereo_compute(self._h, _ptr(L), _ptr(R), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def compute_rgb(self, L_rgb, R_rgb, out, stream=None):
+        """L_rgb, R_rgb: CUDA u8 [H][W][3]; gray front end (§III item 1) + pipeline."""
+        _check(lib().stereo_compute_rgb(self._h, _ptr(L_rgb), _ptr(R_rgb), _ptr(out),
+                                        _stream_ptr(stream)))
         return out
 
     def compute_batch(self, L, R, out, nframes, stream=None):
@@ -266,3 +281,10 @@ def unpack_pix(pix):
 def unpack_arms(arm):
     """u32 m | n<<8 | M<<16 | N<<24 -> u8 [4][H][W] (m, n, M, N)."""
     return np.stack([(arm >> s) & 255 for s in (0, 8, 16, 24)]).astype(np.uint8)
+
+
+def rgb_to_gray(rgb, gray, stream=None):
+    """CUDA u8 [H][W][3] -> CUDA u8 [H][W] (BT.601, §III item 1), enqueued."""
+    H, W = int(rgb.shape[0]), int(rgb.shape[1])
+    _check(lib().stereo_rgb_to_gray(_ptr(rgb), _ptr(gray), W, H, _stream_ptr(stream)))
+    return gray

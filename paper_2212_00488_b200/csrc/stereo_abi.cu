@@ -102,6 +102,7 @@ int validate(int W, int H, int D, const stereo_params* p) {
   if (p->t_fill < 0) return fail(STEREO_EINVAL, "t_fill must be >= 0");
   if (p->w_x < 0) return fail(STEREO_EINVAL, "w_x must be >= 0");
   if (p->w_y < 0) return fail(STEREO_EINVAL, "w_y must be >= 0");
+  if (p->w_x_r < -1) return fail(STEREO_EINVAL, "w_x_r must be -1 (= w_x) or >= 0");
   if (p->k_scale < 1) return fail(STEREO_EINVAL, "k_scale must be >= 1");
   if (D < 1) return fail(STEREO_EINVAL, "D (d_max_org) must be >= 1");
   if (W < 1 || H < 1) return fail(STEREO_EINVAL, "W and H must be >= 1");
@@ -113,12 +114,15 @@ int validate(int W, int H, int D, const stereo_params* p) {
       if (p->census_dx[i] == p->census_dx[j] && p->census_dy[i] == p->census_dy[j])
         return fail(STEREO_EINVAL, "census offsets %d and %d are not distinct", j, i);
   }
+  if (p->fill_mode < STEREO_FILL_BILATERAL || p->fill_mode > STEREO_FILL_EQ11_LITERAL)
+    return fail(STEREO_EINVAL, "fill_mode must be one of STEREO_FILL_*");
   if (p->k_scale > 2) return fail(STEREO_EUNSUPPORTED, "k_scale must be 1 or 2");
   if (W / p->k_scale < 1 || H / p->k_scale < 1)
     return fail(STEREO_EINVAL, "scaled image is empty (W/K or H/K < 1)");
   if ((D + p->k_scale - 1) / p->k_scale > 255)
     return fail(STEREO_EUNSUPPORTED, "ceil(D/K) must be <= 255 (u8 disparity maps)");
-  if (p->w_x > 254 || p->w_y > 254) return fail(STEREO_EUNSUPPORTED, "w_x, w_y must be <= 254");
+  if (p->w_x > 254 || p->w_y > 254 || p->w_x_r > 254)
+    return fail(STEREO_EUNSUPPORTED, "w_x, w_x_r, w_y must be <= 254");
   if (p->m_pool > 3) return fail(STEREO_EUNSUPPORTED, "m_pool must be <= 3");
   for (int i = 0; i < 6; ++i)
     if (p->census_dx[i] < -2 || p->census_dx[i] > 2 || p->census_dy[i] < -2 || p->census_dy[i] > 2)
@@ -237,6 +241,8 @@ void stereo_default_params(stereo_params* p) {
   p->delta = 20;
   p->k_scale = 2;
   p->m_pool = 1;
+  p->w_x_r = -1;
+  p->fill_mode = STEREO_FILL_BILATERAL;
   const int8_t dx[6] = {0, -1, 1, -1, 1, 0}, dy[6] = {-2, -1, -1, 1, 1, 2};
   for (int i = 0; i < 6; ++i) {
     p->census_dx[i] = dx[i];
@@ -260,7 +266,10 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   g.Ws = W / g.K; g.Hs = H / g.K; g.Ds = (D + g.K - 1) / g.K;
   g.Wp = 32 * xpass_chunk_for(g.Ws);  // CA_x pitch = the x pass's lane-chunk span
   g.w_x = p->w_x; g.w_y = p->w_y; g.delta = p->delta; g.t_fill = p->t_fill;
-  g.f = frac_bits(p->w_x);
+  g.w_x_r = p->w_x_r < 0 ? p->w_x : p->w_x_r;
+  g.w_x_max = g.w_x > g.w_x_r ? g.w_x : g.w_x_r;
+  g.fill_mode = p->fill_mode;
+  g.f = frac_bits(g.w_x_max);
   g.border = 1u << (g.f + 1);
   for (int i = 0; i < 6; ++i) { g.cdx[i] = p->census_dx[i]; g.cdy[i] = p->census_dy[i]; }
   if (!xpass_chunk_for(g.Ws)) {
@@ -284,6 +293,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       {(void**)&b.pixL, n * 2}, {(void**)&b.pixR, n * 2}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
       {(void**)&b.xrow, (size_t)4 * g.Hs * g.Wp * 4},
+      {(void**)&b.grayL, (size_t)W * H}, {(void**)&b.grayR, (size_t)W * H},
       {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
       {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
       {(void**)&b.patchVals, (size_t)g.Hs * 4},
@@ -332,6 +342,22 @@ int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_
                    void* stream) {
   if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
   return enqueue_frame(h, L, R, disp_out, (cudaStream_t)stream);
+}
+
+int stereo_rgb_to_gray(const uint8_t* rgb, uint8_t* gray, int W, int H, void* stream) {
+  g_err.clear();
+  if (!rgb || !gray) return fail(STEREO_EINVAL, "NULL buffer");
+  if (W < 1 || H < 1) return fail(STEREO_EINVAL, "W and H must be >= 1");
+  CU(launch_gray(rgb, nullptr, gray, nullptr, W, H, (cudaStream_t)stream));
+  return STEREO_OK;
+}
+
+int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb, float* disp_out,
+                       void* stream) {
+  if (!h || !L_rgb || !R_rgb || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  const cudaStream_t s = (cudaStream_t)stream;
+  CU(launch_gray(L_rgb, R_rgb, h->b.grayL, h->b.grayR, h->g.W, h->g.H, s));
+  return enqueue_frame(h, h->b.grayL, h->b.grayR, disp_out, s);
 }
 
 int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,

@@ -16,6 +16,9 @@ struct Geom {
   int Ws, Hs, Ds;   // scaled sizes
   int Wp;           // row pitch (elements) of the CA_x volumes: Ws rounded up to 32
   int w_x, w_y, delta, t_fill;
+  int w_x_r;        // right-base x arm cap (resolved: >= 0)
+  int w_x_max;      // max(w_x, w_x_r): x halos and the fixed-point width
+  int fill_mode;    // STEREO_FILL_*
   int f;            // fixed-point fraction bits
   uint32_t border;  // 2^(f+1): the BORDER cost (reading R12b)
   int8_t cdx[6], cdy[6];
@@ -51,6 +54,9 @@ struct Buffers {
   uint8_t* inL = nullptr;
   uint8_t* inR = nullptr;
   float* outF = nullptr;
+  // gray front end of stereo_compute_rgb: u8 [H][W] x 2
+  uint8_t* grayL = nullptr;
+  uint8_t* grayR = nullptr;
 };
 
 // Launch configuration chosen at create time.
@@ -83,6 +89,8 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
                          cudaStream_t s);
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
                         float* out, cudaStream_t s);
+cudaError_t launch_gray(const uint8_t* rgb0, const uint8_t* rgb1, uint8_t* g0, uint8_t* g1,
+                        int W, int H, cudaStream_t s);
 cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,
                          const int32_t* rows_dev, const float* vals_dev, int n, cudaStream_t s);
 

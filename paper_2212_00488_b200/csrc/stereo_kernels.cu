@@ -102,7 +102,7 @@ struct PrepArgs {
   uint32_t* arm0;
   uint32_t* arm1;
   uint32_t* xrow;  // [4][Hs][Wp]: x-pass code L, R; window offsets L, R
-  int Ws, Hs, Wp, w_x, w_y, delta;
+  int Ws, Hs, Wp, w_x, w_x_r, w_y, delta;  // w_x: left image (D^L) x cap, w_x_r: right
   int HX, HY, BWp, AHp;  // halos and padded strip pitches
   int8_t cdx[6], cdy[6];
 };
@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   const size_t plane = (size_t)a.Hs * a.Wp;
   const bool big = a.delta >= 128;
   const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
+  const int wx = blockIdx.z ? a.w_x_r : a.w_x;  // per-base x cap
 #pragma unroll 1
   for (int rr = 0; rr < kPrepRows; ++rr) {
     const int ty2 = ty + 8 * rr, y = y0 + ty2;
@@ -204,14 +205,14 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     for (int i = 0; i < 6; ++i) code |= (ctr[a.cdy[i] * BWp + a.cdx[i]] < c) << i;
     int n, m, N, M;
     if (a.delta > 255) {  // |dI| <= 255 < delta: every neighbour is similar
-      n = min(a.w_x, a.Ws - 1 - x); m = min(a.w_x, x);
+      n = min(wx, a.Ws - 1 - x); m = min(wx, x);
       N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
     } else {
       const uint32_t c4 = (uint32_t)c * 0x01010101u;
       const int oB = (ty2 + 2) * BWp + tx + HX + 8;                      // centre in sB
       const int oV = kPrepSB * BWp + (tx + 2) * AHp + ty2 + HY + 8;      // centre in sV
-      n = run_fwd(psm32, oB + 1, min(a.w_x, a.Ws - 1 - x), c4, dl4, big);
-      m = run_bwd(psm32, oB, min(a.w_x, x), c4, dl4, big);
+      n = run_fwd(psm32, oB + 1, min(wx, a.Ws - 1 - x), c4, dl4, big);
+      m = run_bwd(psm32, oB, min(wx, x), c4, dl4, big);
       N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, dl4, big);
       M = run_bwd(psm32, oV, min(a.w_y, y), c4, dl4, big);
     }
@@ -231,7 +232,7 @@ static int prep_rows_for(const Geom& g, int nsm) {
 }
 
 static void prep_geometry(const Geom& g, int pr, int& HX, int& HY, int& BWp, int& AHp) {
-  HX = g.w_x > 2 ? g.w_x : 2;
+  HX = g.w_x_max > 2 ? g.w_x_max : 2;
   HY = g.w_y > 2 ? g.w_y : 2;
   BWp = (32 + 2 * HX + 16 + 15) & ~15;
   AHp = (8 * pr + 2 * HY + 16 + 3) & ~3;
@@ -245,7 +246,8 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
   a.pix0 = b.pixL; a.pix1 = b.pixR;
   a.arm0 = b.armL; a.arm1 = b.armR;
   a.xrow = b.xrow;
-  a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_y = g.w_y; a.delta = g.delta;
+  a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_x_r = g.w_x_r; a.w_y = g.w_y;
+  a.delta = g.delta;
   const int pr = p.prep_rows;
   prep_geometry(g, pr, a.HX, a.HY, a.BWp, a.AHp);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
@@ -492,7 +494,7 @@ constexpr int xpass_nd() { return C <= kXMaxC2 ? 2 : 1; }
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x, g.border};
+          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border};
   xpass_kernel<C, xpass_nd<C>()><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -887,6 +889,7 @@ struct PostArgs {
   int32_t* rowLast;
   unsigned* counter;
   int W, H, Ws, Hs, K, T;
+  int fill_mode;  // STEREO_FILL_*
   int Wsp;  // Ws rounded up to 32
   int Wx;   // W rounded up to 4
 };
@@ -914,13 +917,20 @@ __device__ __forceinline__ float su_xval(const float* f, const uint8_t* __restri
   return av;
 }
 
-// bilateral fill value of pixel x given its nearest valid neighbours li / ri
+// fill value of pixel x given its nearest valid neighbours li / ri (§III.E):
+// mode 0 the bilateral estimation, 1 / 2 the Fig. 6 baselines (nearest /
+// smaller disparity), 3 Eq. 11 as printed -- every rational
+// result rounded once (__fdiv_rn of exact integers, |numerator| < 2^24)
 __device__ __forceinline__ float fill_value(const uint8_t* md, const uint16_t* pix,
-                                            int x, int li, int ri, int T) {
+                                            int x, int li, int ri, int T, int mode) {
   if (li >= 0 && ri >= 0) {
     const int Dl = md[li], Dr = md[ri];
     const int i = x - li, j = ri - x;
-    if (abs(Dl - Dr) <= T) return __fdiv_rn((float)(Dl * j + Dr * i), (float)(i + j));
+    if (mode == 1) return (float)(i <= j ? Dl : Dr);  // equal distances -> left
+    if (mode == 2) return (float)min(Dl, Dr);
+    if (abs(Dl - Dr) <= T)
+      return mode == 3 ? __fdiv_rn((float)(Dl * (i + j) + i * (Dl - Dr)), (float)(i + j))
+                       : __fdiv_rn((float)(Dl * j + Dr * i), (float)(i + j));
     const int cI = pix[x] & 255, lI = pix[li] & 255, rI = pix[ri] & 255;
     return (abs(lI - cI) <= abs(rI - cI)) ? (float)Dl : (float)Dr;
   }
@@ -1109,7 +1119,7 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
         const unsigned above = ln == 31 ? 0u : (m & ~((2u << ln) - 1u));
         const int li = below ? cc * 32 + 31 - __clz(below) : prevLast[j * 64 + cc];
         const int ri = above ? cc * 32 + __ffs(above) - 1 : nextFirst[j * 64 + cc];
-        v = fill_value(mdr, pix, x, li, ri, a.T);
+        v = fill_value(mdr, pix, x, li, ri, a.T, a.fill_mode);
       }
       fv[j * Wsp + x] = v;
       if (j < nr) (a.K == 2 ? a.fill : a.out)[(size_t)(y0 + j) * Ws + x] = v;
@@ -1221,6 +1231,7 @@ cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* 
   a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
   a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
+  a.fill_mode = g.fill_mode;
   a.Wsp = (g.Ws + 31) & ~31;
   a.Wx = (g.W + 3) & ~3;
   patch_kernel<<<1, 256, 0, s>>>(a, rows_dev, vals_dev, n);
@@ -1234,12 +1245,39 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
   a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
+  a.fill_mode = g.fill_mode;
   a.Wsp = (g.Ws + 31) & ~31;
   a.Wx = (g.W + 3) & ~3;
   const int R = p.post_rows, nt = p.post_threads;
   if (R == 1) post_kernel<1><<<g.Hs, nt, p.post_smem, s>>>(a);
   else if (R == 2) post_kernel<2><<<(g.Hs + 1) / 2, nt, p.post_smem, s>>>(a);
   else post_kernel<4><<<(g.Hs + 3) / 4, nt, p.post_smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// GRAY — §III list item 1, BT.601 luma rounded half up (reading R31,
+// S:117): floor((299 R + 587 G + 114 B + 500) / 1000), exact integers.
+// rgb u8 [H][W][3] -> u8 [H][W]; blockIdx.y selects the image (L / R).
+// ============================================================================
+__global__ void __launch_bounds__(256) gray_kernel(const uint8_t* __restrict__ rgb0,
+                                                   const uint8_t* __restrict__ rgb1,
+                                                   uint8_t* __restrict__ g0,
+                                                   uint8_t* __restrict__ g1, int n) {
+  const uint8_t* rgb = blockIdx.y ? rgb1 : rgb0;
+  uint8_t* g = blockIdx.y ? g1 : g0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t r = __ldg(rgb + 3 * (size_t)k), gg = __ldg(rgb + 3 * (size_t)k + 1),
+                   b = __ldg(rgb + 3 * (size_t)k + 2);
+    g[k] = (uint8_t)((299u * r + 587u * gg + 114u * b + 500u) / 1000u);
+  }
+}
+
+cudaError_t launch_gray(const uint8_t* rgb0, const uint8_t* rgb1, uint8_t* g0, uint8_t* g1,
+                        int W, int H, cudaStream_t s) {
+  const int n = W * H;
+  const int blocks = std::min((n + 255) / 256, 148 * 8);
+  gray_kernel<<<dim3(blocks, rgb1 ? 2 : 1), 256, 0, s>>>(rgb0, rgb1, g0, g1, n);
   return cudaGetLastError();
 }
 
@@ -1312,7 +1350,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
-  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x + 3;
+  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
   {
     const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
     const size_t fixed = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 +

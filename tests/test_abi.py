@@ -46,6 +46,7 @@ def test_default_params_are_the_papers():
     assert (p.w_x, p.w_y, p.k_scale, p.m_pool) == (21, 31, 2, 1)
     assert p.delta == 20                                           # S:90 (reading R13)
     assert list(zip(p.census_dx, p.census_dy)) == [(0, -2), (-1, -1), (1, -1), (-1, 1), (1, 1), (0, 2)]
+    assert (p.w_x_r, p.fill_mode) == (-1, abi.FILL_BILATERAL)      # NEXT-3 variants off
 
 
 def _create(W=64, H=48, D=16, **kw):
@@ -66,6 +67,10 @@ def _create(W=64, H=48, D=16, **kw):
     (dict(k_scale=3), abi.STEREO_EUNSUPPORTED, "k_scale must be 1 or 2"),
     (dict(w_x=255), abi.STEREO_EUNSUPPORTED, "254"),
     (dict(m_pool=4), abi.STEREO_EUNSUPPORTED, "m_pool"),
+    (dict(w_x_r=-2), abi.STEREO_EINVAL, "w_x_r"),
+    (dict(w_x_r=255), abi.STEREO_EUNSUPPORTED, "254"),
+    (dict(fill_mode=4), abi.STEREO_EINVAL, "fill_mode"),
+    (dict(fill_mode=-1), abi.STEREO_EINVAL, "fill_mode"),
     (dict(abi_version=7), abi.STEREO_EINVAL, "abi_version"),
     (dict(census=[(0, -2), (0, -2), (1, -1), (-1, 1), (1, 1), (0, 2)]), abi.STEREO_EINVAL, "distinct"),
     (dict(census=[(0, 0), (-1, -1), (1, -1), (-1, 1), (1, 1), (0, 2)]), abi.STEREO_EINVAL, "zero"),
@@ -94,6 +99,8 @@ def test_null_arguments():
     assert L.stereo_create(8, 8, 4, None, C.byref(C.c_void_p())) == abi.STEREO_EINVAL
     assert L.stereo_compute(None, None, None, None, None) == abi.STEREO_EINVAL
     assert L.stereo_get_info(None, None) == abi.STEREO_EINVAL
+    assert L.stereo_compute_rgb(None, None, None, None, None) == abi.STEREO_EINVAL
+    assert L.stereo_rgb_to_gray(None, None, 4, 4, None) == abi.STEREO_EINVAL
     L.stereo_destroy(None)  # no-op
 
 

@@ -117,6 +117,10 @@ def test_random_small_instances(seed):
     kw = dict(k_scale=K, delta=int(rng.integers(1, 60)), w_x=int(rng.integers(0, 30)),
               w_y=int(rng.integers(0, 40)), t_fill=int(rng.integers(0, 6)),
               m_pool=int(rng.integers(0, 3)), census=pat)
+    if rng.random() < 0.3:  # NEXT-3 variants: right-base x cap, fill modes
+        kw["w_x_r"] = int(rng.integers(0, 30))
+    if rng.random() < 0.4:
+        kw["fill_mode"] = int(rng.integers(0, 4))
     kind = rng.integers(0, 3)
     if kind == 0:
         L, R = synth.random_pair(W, H, seed, levels=int(rng.choice([2, 8, 256])))
@@ -232,6 +236,43 @@ def test_ca_volume_split_prefix_extremes(case):
 def test_next2_workloads_bit_exact(W, H, D):
     L, R, _ = synth.scene(W, H, D, seed=3)
     _compare(L, R, D, dict(), volumes=False)
+
+
+@pytest.mark.parametrize("mode", ["bilateral", "nearest", "smaller", "eq11_literal"])
+def test_next3_fill_modes_bit_exact(mode):
+    """NEXT-3: the Fig. 6 baselines and the printed Eq. 11 (§III.E), c2 scene
+    (many occlusion non-GCPs) with K = 2 so the scale-up sees every mode."""
+    L, R, _ = synth.scene(450, 376, 64, seed=12)
+    _compare(L, R, 64, dict(fill_mode=oracle.FILL_MODES[mode]), volumes=False)
+
+
+@pytest.mark.parametrize("w_x,w_x_r", [(21, 5), (7, 41), (0, 21)])
+def test_next3_asymmetric_x_windows_bit_exact(w_x, w_x_r):
+    """NEXT-3: different x aggregation caps for D^L and D^R."""
+    L, R, _ = synth.scene(300, 160, 48, seed=w_x + w_x_r)
+    got, ref = _compare(L, R, 48, dict(k_scale=1, w_x=w_x, w_x_r=w_x_r))
+    assert got["armR"][0].max() <= w_x_r and got["armL"][0].max() <= w_x
+
+
+def test_rgb_front_end_bit_exact():
+    """§III item 1: gray front end + pipeline == oracle(rgb_to_gray)."""
+    W, H, D = 320, 200, 48
+    L, R, _ = synth.scene(W, H, D, seed=21)
+    rng = np.random.default_rng(5)
+    # colour images whose luma is not the gray scene: the conversion matters
+    Lrgb = np.clip(L[..., None].astype(np.int32) + rng.integers(-40, 41, (H, W, 3)), 0, 255).astype(np.uint8)
+    Rrgb = np.clip(R[..., None].astype(np.int32) + rng.integers(-40, 41, (H, W, 3)), 0, 255).astype(np.uint8)
+    gL, gR = oracle.rgb_to_gray(Lrgb), oracle.rgb_to_gray(Rrgb)
+    ref = oracle.pipeline(gL, gR, D, oracle.params(), "fixed", stages=("out",))["out"]
+    st = abi.Stereo(W, H, D)
+    out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    st.compute_rgb(torch.from_numpy(Lrgb).to(DEV), torch.from_numpy(Rrgb).to(DEV), out)
+    g = torch.zeros((H, W), dtype=torch.uint8, device=DEV)
+    abi.rgb_to_gray(torch.from_numpy(Lrgb).to(DEV), g)
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cpu().numpy(), gL)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    st.close()
 
 
 def test_disparity_maps_vs_double_definition():
