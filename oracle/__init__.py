@@ -120,6 +120,7 @@ def lib():
                 "or_median3x3": (None, [u8p, C.c_int, C.c_int, u8p]),
                 "or_fill_bilateral": (None, [u8p, u8p, C.c_int, C.c_int, C.c_int, C.c_int, f32p]),
                 "or_rgb_to_gray": (None, [u8p, C.c_int, C.c_int, u8p]),
+                "or_depth": (None, [f32p, C.c_int, C.c_float, f32p]),
                 "or_scale_up": (None, [f32p, C.c_int, C.c_int, u8p, C.c_int, C.c_int, C.c_int,
                                        C.c_int, f32p]),
                 "or_pipeline": (C.c_int, [u8p, u8p, C.c_int, C.c_int, C.c_int, C.POINTER(Params),
@@ -270,6 +271,14 @@ def fill_bilateral(med, Limg, T=3, mode=0):
     out = np.zeros((H, W), np.float32)
     mode = FILL_MODES[mode] if isinstance(mode, str) else mode
     lib().or_fill_bilateral(med, Limg, W, H, T, mode, out)
+    return out
+
+
+def depth(disp, fB):
+    """Eq. 1 (P:103-108): Z = fl32(fB / d), d = 0 -> +inf."""
+    disp = np.ascontiguousarray(disp, dtype=np.float32)
+    out = np.zeros_like(disp)
+    lib().or_depth(disp.reshape(-1), disp.size, fB, out.reshape(-1))
     return out
 
 

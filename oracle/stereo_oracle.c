@@ -383,6 +383,10 @@ void or_rgb_to_gray(const uint8_t* rgb, int W, int H, uint8_t* gray) {
   }
 }
 
+void or_depth(const float* disp, int n, float fB, float* Z) {
+  for (int k = 0; k < n; ++k) Z[k] = disp[k] > 0.0f ? fB / disp[k] : INFINITY;
+}
+
 /* Step8: scale up x K (K = 2), bilateral along x (the §III.E rule
  * again, with i = j = 1), linear along y.  Readings: R27 values scaled by K
  * (S:449); R28 threshold K*T; R29 seeds on the even grid, x

@@ -120,6 +120,9 @@ void or_fill_bilateral(const uint8_t* med, const uint8_t* Limg, int W, int H, in
  * unstated -> BT.601 luma, round half up (reading R31):
  * gray = floor((299 R + 587 G + 114 B + 500) / 1000); rgb is [H][W][3] */
 void or_rgb_to_gray(const uint8_t* rgb, int W, int H, uint8_t* gray);
+/* Eq. 1: Z = f B / d, d = 0 -> +infinity ("at infinity",
+ * P:107-108); fB = f*B given as one binary32 value, Z = fl32(fB / d) */
+void or_depth(const float* disp, int n, float fB, float* Z);
 /* Step8 */
 void or_scale_up(const float* v, int Ws, int Hs, const uint8_t* Lorg, int W, int H,
                  int K, int T, float* out);

@@ -413,3 +413,13 @@ def test_right_base_arm_cap():
     assert r["armL"][0].max() == 5 and r["armL"][1].max() == 5
     assert r["armR"][0].max() == 2 and r["armR"][1].max() == 2
     assert np.array_equal(r["armL"][2:], r["armR"][2:])
+
+
+def test_depth_eq1():
+    """Eq. 1: Z = f B / d; d = 0 is 'at infinity'."""
+    d = np.array([[2.0, 0.0, 3.0, 0.5, 144.0]], np.float32)
+    Z = oracle.depth(d, 10.0)
+    assert Z[0, 0] == 5.0 and np.isinf(Z[0, 1]) and Z[0, 1] > 0
+    assert Z[0, 2] == np.float32(10.0) / np.float32(3.0) and Z[0, 3] == 20.0
+    # smaller d -> farther (P:106-107)
+    assert Z[0, 4] < Z[0, 2] < Z[0, 0]
