@@ -215,6 +215,14 @@ int stereo_rgb_to_gray(const uint8_t* rgb, uint8_t* gray, int W, int H, void* st
 int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb,
                        float* disp_out, void* stream);
 
+/* Depth from disparity, Eq. 1: Z = f B / d with fB = f*B given
+ * as one binary32 value; Z = fl32(fB / d) (one correctly rounded division),
+ * d <= 0 -> +infinity ("d = 0 means that the object is at infinity",
+ * P:107-108).  disp, Z: DEVICE f32 [n] (e.g. disp_out of stereo_compute,
+ * n = W*H; Z may alias disp); enqueued on `stream`.  STEREO_EINVAL for NULL
+ * pointers or n < 0. */
+int stereo_disparity_to_depth(const float* disp, float* Z, int n, float fB, void* stream);
+
 /* Row-band support.  A band of a frame is computed by running
  * the normal pipeline on a sub-image whose halo rows cover the dependency cone
  * of the band's own rows; only rule (d) of the fill (a row without any valid

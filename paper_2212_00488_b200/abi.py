@@ -39,7 +39,7 @@ EXPORTS = (
     "stereo_compute_host", "stereo_destroy", "stereo_last_error", "stereo_get_info",
     "stereo_get_tables", "stereo_debug_download", "stereo_debug_upload", "stereo_set_debug",
     "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms", "stereo_patch_rows",
-    "stereo_rgb_to_gray", "stereo_compute_rgb",
+    "stereo_rgb_to_gray", "stereo_compute_rgb", "stereo_disparity_to_depth",
 )
 
 
@@ -112,6 +112,7 @@ def lib():
             "stereo_patch_rows": (i32, [vp, vp, vp, i32, vp, vp, vp]),
             "stereo_rgb_to_gray": (i32, [vp, vp, i32, i32, vp]),
             "stereo_compute_rgb": (i32, [vp, vp, vp, vp, vp]),
+            "stereo_disparity_to_depth": (i32, [vp, vp, i32, C.c_float, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -288,3 +289,10 @@ def rgb_to_gray(rgb, gray, stream=None):
     H, W = int(rgb.shape[0]), int(rgb.shape[1])
     _check(lib().stereo_rgb_to_gray(_ptr(rgb), _ptr(gray), W, H, _stream_ptr(stream)))
     return gray
+
+
+def disparity_to_depth(disp, Z, fB, stream=None):
+    """Eq. 1: CUDA f32 disparities -> CUDA f32 depth Z = fB / d (d <= 0 -> inf)."""
+    _check(lib().stereo_disparity_to_depth(_ptr(disp), _ptr(Z), int(disp.numel()), float(fB),
+                                           _stream_ptr(stream)))
+    return Z

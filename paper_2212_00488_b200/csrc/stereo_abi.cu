@@ -352,6 +352,14 @@ int stereo_rgb_to_gray(const uint8_t* rgb, uint8_t* gray, int W, int H, void* st
   return STEREO_OK;
 }
 
+int stereo_disparity_to_depth(const float* disp, float* Z, int n, float fB, void* stream) {
+  g_err.clear();
+  if (!disp || !Z) return fail(STEREO_EINVAL, "NULL buffer");
+  if (n < 0) return fail(STEREO_EINVAL, "n must be >= 0");
+  CU(launch_depth(disp, Z, n, fB, (cudaStream_t)stream));
+  return STEREO_OK;
+}
+
 int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb, float* disp_out,
                        void* stream) {
   if (!h || !L_rgb || !R_rgb || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");

@@ -89,6 +89,7 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
                          cudaStream_t s);
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
                         float* out, cudaStream_t s);
+cudaError_t launch_depth(const float* disp, float* Z, int n, float fB, cudaStream_t s);
 cudaError_t launch_gray(const uint8_t* rgb0, const uint8_t* rgb1, uint8_t* g0, uint8_t* g1,
                         int W, int H, cudaStream_t s);
 cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,

@@ -1282,6 +1282,24 @@ cudaError_t launch_gray(const uint8_t* rgb0, const uint8_t* rgb1, uint8_t* g0, u
 }
 
 // ============================================================================
+// DEPTH — Eq. 1: Z = fl32(fB / d), d <= 0 -> +infinity
+// ============================================================================
+__global__ void __launch_bounds__(256) depth_kernel(const float* disp, float* Z, int n,
+                                                    float fB) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const float d = disp[k];
+    Z[k] = d > 0.0f ? __fdiv_rn(fB, d) : __int_as_float(0x7f800000);
+  }
+}
+
+cudaError_t launch_depth(const float* disp, float* Z, int n, float fB, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = std::min((n + 255) / 256, 148 * 8);
+  depth_kernel<<<blocks, 256, 0, s>>>(disp, Z, n, fB);
+  return cudaGetLastError();
+}
+
+// ============================================================================
 // Launch planning (create time)
 // ============================================================================
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,

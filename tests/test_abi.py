@@ -101,6 +101,7 @@ def test_null_arguments():
     assert L.stereo_get_info(None, None) == abi.STEREO_EINVAL
     assert L.stereo_compute_rgb(None, None, None, None, None) == abi.STEREO_EINVAL
     assert L.stereo_rgb_to_gray(None, None, 4, 4, None) == abi.STEREO_EINVAL
+    assert L.stereo_disparity_to_depth(None, None, 4, 1.0, None) == abi.STEREO_EINVAL
     L.stereo_destroy(None)  # no-op
 
 

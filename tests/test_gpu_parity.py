@@ -275,6 +275,21 @@ def test_rgb_front_end_bit_exact():
     st.close()
 
 
+def test_depth_eq1_bit_exact():
+    """NEXT-4: Eq. 1 on a computed disparity map (d = 0 -> +inf)."""
+    L, R, _ = synth.scene(200, 120, 32, seed=4)
+    st = abi.Stereo(200, 120, 32)
+    out = torch.zeros((120, 200), dtype=torch.float32, device=DEV)
+    st.compute(torch.from_numpy(L).to(DEV), torch.from_numpy(R).to(DEV), out)
+    out[0, :5] = torch.tensor([0.0, 1.0, 3.0, 0.5, 144.0])
+    Z = torch.empty_like(out)
+    abi.disparity_to_depth(out, Z, 1234.5)
+    torch.cuda.synchronize()
+    ref = oracle.depth(out.cpu().numpy(), 1234.5)
+    assert np.array_equal(Z.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    st.close()
+
+
 def test_disparity_maps_vs_double_definition():
     """<= 0.01% of D^L/D^R pixels may differ from the double-mode oracle, and
     only where the two candidates' double costs tie within 1e-5 (north_star)."""
