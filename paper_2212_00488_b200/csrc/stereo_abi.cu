@@ -290,11 +290,11 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
   Buffers& b = h->b;
   struct A { void** p; size_t bytes; } as[] = {
-      {(void**)&b.pixL, n * 2}, {(void**)&b.pixR, n * 2}, {(void**)&b.armL, n * 4},
+      {(void**)&b.pixL, n * 2 + 16}, {(void**)&b.pixR, n * 2 + 16}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
       {(void**)&b.xrow, (size_t)4 * g.Hs * g.Wp * 4},
       {(void**)&b.grayL, (size_t)W * H}, {(void**)&b.grayR, (size_t)W * H},
-      {(void**)&b.DL, n}, {(void**)&b.DR, n}, {(void**)&b.masked, n}, {(void**)&b.median, n},
+      {(void**)&b.DL, n + 16}, {(void**)&b.DR, n + 16}, {(void**)&b.masked, n}, {(void**)&b.median, n},
       {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
       {(void**)&b.patchVals, (size_t)g.Hs * 4},
       {(void**)&b.counter, 16},

@@ -974,6 +974,23 @@ __device__ void su_row_global(const PostArgs& a, int Y, float thr) {
   }
 }
 
+// n bytes from global src (any alignment) to 4-byte aligned shared dst with
+// one aligned word load (+ its successor, when misaligned) and one word store
+// per 4 bytes; reads up to 7 bytes past src + n when src is misaligned
+__device__ __forceinline__ void stage_row(uint8_t* dst, const uint8_t* src, int n, int tid,
+                                          int nthreads) {
+  const uintptr_t ad = reinterpret_cast<uintptr_t>(src);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~(uintptr_t)3);
+  const int sh = 8 * (int)(ad & 3);
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  const int nw = (n + 3) >> 2;
+  if (sh == 0) {
+    for (int t = tid; t < nw; t += nthreads) d[t] = __ldg(w + t);
+  } else {
+    for (int t = tid; t < nw; t += nthreads) d[t] = __funnelshift_r(__ldg(w + t), __ldg(w + t + 1), sh);
+  }
+}
+
 template <int R>  // scaled rows owned per CTA
 __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   extern __shared__ uint32_t psm_[];
@@ -996,21 +1013,25 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   const int nf = a.K == 2 ? min(nr + 1, a.Hs - y0) : nr;     // fill rows needed (SU reads y+1)
   const float thr = (float)(a.K * a.T);
 
-  // 0. stage every input row in shared memory: one batch of independent loads
+  // 0. stage every input row in shared memory: one batch of independent
+  // word loads (rows are re-aligned with a funnel shift; the handle's own
+  // buffers carry 16 bytes of tail padding for the over-read)
   for (int r = 0; r < nf + 2; ++r) {
     const size_t o = (size_t)clampi(y0 - 1 + r, 0, a.Hs - 1) * Ws;
-#pragma unroll 4
-    for (int x = tid; x < Ws; x += blockDim.x) {
-      sDL[r * Wsp + x] = __ldg(a.DL + o + x);
-      sDR[r * Wsp + x] = __ldg(a.DR + o + x);
-    }
+    stage_row(sDL + r * Wsp, a.DL + o, Ws, tid, blockDim.x);
+    stage_row(sDR + r * Wsp, a.DR + o, Ws, tid, blockDim.x);
   }
   for (int j = 0; j < nf; ++j) {
-#pragma unroll 4
-    for (int x = tid; x < Ws; x += blockDim.x) sPix[j * Wsp + x] = __ldg(a.pixL + (size_t)(y0 + j) * Ws + x);
+    stage_row(reinterpret_cast<uint8_t*>(sPix + j * Wsp),
+              reinterpret_cast<const uint8_t*>(a.pixL + (size_t)(y0 + j) * Ws), 2 * Ws, tid,
+              blockDim.x);
     if (a.K == 2) {
-#pragma unroll 4
-      for (int X = tid; X < W; X += blockDim.x) sLo[j * Wx + X] = __ldg(a.Lorg + (size_t)(2 * (y0 + j)) * W + X);
+      const uint8_t* src = a.Lorg + (size_t)(2 * (y0 + j)) * W;
+      if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)W) & 3) == 0) {  // caller buffer:
+        stage_row(sLo + j * Wx, src, W, tid, blockDim.x);                // no over-read
+      } else {
+        for (int X = tid; X < W; X += blockDim.x) sLo[j * Wx + X] = __ldg(src + X);
+      }
     }
   }
   __syncthreads();
