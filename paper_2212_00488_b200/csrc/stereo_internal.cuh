@@ -66,6 +66,7 @@ struct Plan {
   int xpass_smem = 0;
   int xpass_PL = 0;  // per-warp prefix buffer length
   int xpass_warps = 0;
+  int xpass_slots = 3;  // row slots of the bulk-copy ring
   int ypass_B = 0;   // output rows per tile (<= 8*kYRPT)
   int ypass_nb = 0;  // tiles per column strip
   int ypass_SEG = 0; // tile rows per warp; TMA box height = 8*SEG

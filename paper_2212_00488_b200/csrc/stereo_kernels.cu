@@ -270,9 +270,9 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
 // Persistent: one CTA per SM owns a contiguous range of work items
 // (row y, disparity group of ND); every warp takes items independently.  The
 // four PREP row arrays of a row (codes, window offsets; pitch Wp) arrive by
-// bulk asynchronous copies into a ring of kXSlots row slots, completed on an
+// bulk asynchronous copies into a ring of `slots` row slots, completed on an
 // mbarrier; the warp that finishes the last item of a row in the range
-// refills its slot with the row kXSlots ahead, so row loads overlap compute
+// refills its slot with the row `slots` ahead, so row loads overlap compute
 // and no CTA-wide barrier is needed after the start.  Per item:
 //   phase A: lane l scans its contiguous chunk [lC, lC+C) (C odd -> shared
 //            loads at stride C are bank-conflict free); costs from the fixed
@@ -296,10 +296,11 @@ struct XArgs {
   uint32_t* caxR;
   int Ws, Hs, Ds, Wp, PL, ext;
   uint32_t border;
+  int slots;  // row slots in the ring (2..kXMaxSlots)
 };
 
 constexpr int kXMaxWarps = 16;
-constexpr int kXSlots = 3;
+constexpr int kXMaxSlots = 4;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -338,11 +339,12 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   extern __shared__ __align__(128) uint32_t xsm[];
   uint32_t* sQAD = xsm;                // [256][32]  Q_AD[|dI|], one copy per bank
   uint32_t* sQMC = sQAD + 256 * 32;    // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
-  uint32_t* ring = sQMC + 64 * 32;     // [kXSlots][4][32C] row slots
+  uint32_t* ring = sQMC + 64 * 32;     // [slots][4][32C] row slots
   const int nw = blockDim.x >> 5;
-  uint32_t* Pall = ring + kXSlots * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
-  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * a.PL);  // [kXSlots]
-  unsigned* done = reinterpret_cast<unsigned*>(full + kXSlots);                // [kXSlots]
+  const int nslot = a.slots;
+  uint32_t* Pall = ring + nslot * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * a.PL);  // [slots]
+  unsigned* done = reinterpret_cast<unsigned*>(full + kXMaxSlots);             // [slots]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* P = Pall + warp * ND * a.PL;
 
@@ -356,12 +358,12 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   const int skip0 = i0 - rfirst * npairs;  // items of the first row owned by earlier CTAs
 
   if (threadIdx.x == 0) {
-    for (int k = 0; k < kXSlots; ++k) {
+    for (int k = 0; k < nslot; ++k) {
       xbar_init(full + k);
       done[k] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = 0; k < kXSlots && rfirst + k <= rlast; ++k)
+    for (int k = 0; k < nslot && rfirst + k <= rlast; ++k)
       xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
   }
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sQAD[i] = __ldg(a.qad + (i >> 5));
@@ -379,8 +381,8 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
 #pragma unroll 1
   for (int it = i0 + warp; it < i1; it += nw) {
     const int y = it / npairs, d = (it - y * npairs) * ND;
-    const int rel = y - rfirst, slot = rel % kXSlots;
-    xbar_wait(full + slot, (uint32_t)(rel / kXSlots) & 1u);
+    const int rel = y - rfirst, lap = rel / nslot, slot = rel - lap * nslot;
+    xbar_wait(full + slot, (uint32_t)lap & 1u);
     const uint32_t* sL = ring + slot * 4 * 32 * C;
     const uint32_t* sR = sL + 32 * C;
     const uint32_t* sAL = sR + 32 * C;
@@ -466,15 +468,15 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     }
     __syncwarp();
     // ---- release the row slot: the warp finishing the row's last item of
-    // this range refills the slot with the row kXSlots ahead
+    // this range refills the slot with the row `slots` ahead
     if (lane == 0) {
       __threadfence_block();
-      const unsigned target = (unsigned)((rel / kXSlots + 1) * npairs - (slot == 0 ? skip0 : 0));
+      const unsigned target = (unsigned)((lap + 1) * npairs - (slot == 0 ? skip0 : 0));
       const unsigned prev = atomicAdd(done + slot, 1u);
-      if (prev + 1u == target && y + kXSlots <= rlast) {
+      if (prev + 1u == target && y + nslot <= rlast) {
         __threadfence_block();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + kXSlots);
+        xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + nslot);
       }
     }
   }
@@ -494,7 +496,7 @@ constexpr int xpass_nd() { return C <= kXMaxC2 ? 2 : 1; }
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border};
+          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots};
   xpass_kernel<C, xpass_nd<C>()><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1349,6 +1351,14 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Development knobs (plan overrides for tuning experiments; unset = the
+// planner's choice).  Out-of-range values are clamped.
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::max(lo, std::min(hi, std::atoi(v)));
+}
+
 cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
@@ -1386,31 +1396,15 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     }
     if (e != cudaSuccess) return e;
   }
-  // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
-  p.xpass_C = xpass_chunk_for(g.Ws);
-  if (!p.xpass_C) return cudaErrorInvalidValue;
-  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
-  {
-    const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
-    const size_t fixed = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 +
-                                             (size_t)kXSlots * 4 * 32 * p.xpass_C) +
-                         kXSlots * (8 + 4);
-    const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
-    const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
-    if (fixed + per_warp > cap) return cudaErrorInvalidConfiguration;
-    p.xpass_warps = (int)std::min<size_t>(kXMaxWarps, (cap - fixed) / per_warp);
-    p.xpass_smem = (int)(fixed + per_warp * p.xpass_warps);
-    XPASS_DISPATCH(p.xpass_C, e = setup_xpass_c<CC>(p.xpass_smem));
-    if (e != cudaSuccess) return e;
-    p.xpass_grid = nsm;
-  }
   // YPASS: choose the number of tiles per strip balancing halo cost and waves
   // (per-CTA shared wavefronts per d ~ 1.25*TB + 1.75*B + tot exchange)
   const int strips = (g.Ws + 15) / 16;
   const int nb0 = (g.Hs + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
   p.ypass_nb = 0;
+  const int nb_force = env_int("STEREO_YPASS_NB", 0, 0, g.Hs);
   for (int nb = nb0; nb <= g.Hs; ++nb) {
+    if (nb_force && nb != nb_force) continue;
     const int B = (g.Hs + nb - 1) / nb;
     const int SEG = ypass_seg_for(B + 2 * g.w_y);
     if (!SEG) continue;
@@ -1433,6 +1427,37 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        p.ypass_smem));
   if (e != cudaSuccess) return e;
+  // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
+  p.xpass_C = xpass_chunk_for(g.Ws);
+  if (!p.xpass_C) return cudaErrorInvalidValue;
+  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
+  {
+    const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
+    // Co-residency: with frames in flight on several streams, an x pass of one
+    // frame and a y pass of another share each SM when one x-pass CTA of 8
+    // warps with a 2-slot ring fits beside one y-pass CTA (registers: 8 + 8
+    // warps of <= 128; shared memory: both footprints + the per-CTA reserve).
+    // Measured at c3: 143.5 vs 148 us per frame with 6 frames in flight
+    // (16 warps / 3 slots alone); a lone frame is ~5% slower.
+    const int nd0 = p.xpass_C <= kXMaxC2 ? 2 : 1;
+    const size_t co = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)2 * 4 * 32 * p.xpass_C +
+                                          (size_t)8 * nd0 * p.xpass_PL) +
+                      kXMaxSlots * (8 + 4);
+    const bool coresident = co + (size_t)p.ypass_smem + 2 * 1024 <= (size_t)prop.sharedMemPerMultiprocessor;
+    p.xpass_slots = env_int("STEREO_XPASS_SLOTS", coresident ? 2 : 3, 2, kXMaxSlots);
+    const size_t fixed = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 +
+                                             (size_t)p.xpass_slots * 4 * 32 * p.xpass_C) +
+                         kXMaxSlots * (8 + 4);
+    const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
+    const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
+    if (fixed + per_warp > cap) return cudaErrorInvalidConfiguration;
+    p.xpass_warps = (int)std::min<size_t>(kXMaxWarps, (cap - fixed) / per_warp);
+    p.xpass_warps = std::min(p.xpass_warps, env_int("STEREO_XPASS_WARPS", coresident ? 8 : kXMaxWarps, 1, kXMaxWarps));
+    p.xpass_smem = (int)(fixed + per_warp * p.xpass_warps);
+    XPASS_DISPATCH(p.xpass_C, e = setup_xpass_c<CC>(p.xpass_smem));
+    if (e != cudaSuccess) return e;
+    p.xpass_grid = nsm;
+  }
   if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG, 2))) return e;
   if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG, 2))) return e;
   return cudaSuccess;
