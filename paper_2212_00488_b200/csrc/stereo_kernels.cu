@@ -573,6 +573,7 @@ struct YArgs {
   uint64_t* ca0;  // debug (may be null)
   uint64_t* ca1;
   int Ws, Hs, Ds, w_y, B;
+  uint32_t e52;  // kYExp52
 };
 
 constexpr int kYThreads = 256;
@@ -627,7 +628,8 @@ constexpr int kYSplit = 24;  // = byte 3: the hi parts are extracted by byte per
 // with the exponent bits 0x433 (2^52) already OR-ed in (hi < 2^16 + 2^8).
 constexpr uint32_t kYExp52 = 0x43300000u;
 __device__ __forceinline__ void ypass_take(double& best, uint32_t lo, uint32_t hib, int d) {
-  const uint32_t klo = (lo << 8) | (uint32_t)d;
+  uint32_t klo;  // lo << 8 | d as one multiply-add (d < 256)
+  asm("mad.lo.u32 %0, %1, 256, %2;" : "=r"(klo) : "r"(lo), "r"(d));
   const uint32_t khi = (lo >> 24) + hib;
   const double kd = __hiloint2double((int)khi, (int)klo);
   if (kd < best) best = kd;  // never NaN: no fmin NaN fix-ups
@@ -649,7 +651,9 @@ __device__ __forceinline__ void ypass_wta(double (&best)[kYRPT], const uint32_t 
     const uint2 lb = *reinterpret_cast<const uint2*>(EloB + ib);
     const uint32_t dh = *reinterpret_cast<const uint32_t*>(EhiB + (ib >> 1)) -
                         *reinterpret_cast<const uint32_t*>(EhiB + (ia >> 1));
-    ypass_take(best[r], lb.x - la.x, (dh & 0xffffu) | e52, d);
+    uint32_t hib0;  // (dh & 0xffff) | e52 as one three-input logic op
+    asm("lop3.b32 %0, %1, 0xffff, %2, 0xea;" : "=r"(hib0) : "r"(dh), "r"(e52));
+    ypass_take(best[r], lb.x - la.x, hib0, d);
     if (TWO) ypass_take(best[r], lb.y - la.y, (dh >> 16) + e52, d + 1);
   }
 }
@@ -657,10 +661,11 @@ __device__ __forceinline__ void ypass_wta(double (&best)[kYRPT], const uint32_t 
 template <bool TWO>
 __device__ __forceinline__ void ypass_wta_n(int nr, double (&best)[kYRPT],
                                             const uint32_t (&oab)[kYRPT], const uint8_t* EloB,
-                                            const uint8_t* EhiB, int d) {
-  uint32_t z, e52;  // opaque: keeps the optimiser from re-associating the exponent bits
+                                            const uint8_t* EhiB, int d, uint32_t e52) {
+  uint32_t z;  // opaque zero (see ypass_wta)
   asm volatile("mov.u32 %0, 0;" : "=r"(z));
-  asm volatile("mov.u32 %0, %1;" : "=r"(e52) : "n"(kYExp52));
+  // e52 (= kYExp52) arrives as a kernel parameter so that it sits in a
+  // register: the hi-word builds are then single three-input ops
   switch (nr) {  // warp-uniform (depends on the row segment only)
     case 12: ypass_wta<12, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
     case 11: ypass_wta<11, TWO>(best, oab, EloB, EhiB, z, e52, d); break;
@@ -805,9 +810,9 @@ __global__ void __launch_bounds__(kYThreads, 2)
     }
     __syncthreads();  // (2) column prefixes complete
     if (d + 1 < Ds)
-      ypass_wta_n<true>(nrw, best, oab, EloB, EhiB, d);
+      ypass_wta_n<true>(nrw, best, oab, EloB, EhiB, d, a.e52);
     else
-      ypass_wta_n<false>(nrw, best, oab, EloB, EhiB, d);
+      ypass_wta_n<false>(nrw, best, oab, EloB, EhiB, d, a.e52);
     if (DBG) ypass_debug_store(oab, nr, EloB, EhiB, d, d + 1 < Ds, cadbg, a.Hs, a.Ws, y0 + seg, x);
   }
 #pragma unroll
@@ -848,6 +853,7 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
+  a.e52 = kYExp52;
   dim3 grid((g.Ws + 15) / 16, p.ypass_nb, 2);
   cudaError_t e = cudaErrorInvalidValue;
   if (store_ca)
