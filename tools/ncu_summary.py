@@ -27,7 +27,7 @@ want = [
 ]
 idx = {h: i for i, h in enumerate(hdr)}
 for r in rows[2:]:
-    name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")[:26]
+    name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "").replace("stereo::", "")[:26]
     out = [name]
     for m, short in want:
         if m in idx:

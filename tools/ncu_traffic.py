@@ -8,7 +8,7 @@ out = {"source": f"ncu --set full --clock-control none, report {os.path.basename
        "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch; writes still dirty in L2 at kernel end are not counted"}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
-    key = next((k for k in ("sd", "prep", "xpass", "ypass", "post") if name.replace("void ", "").startswith(k)), None)
+    key = next((k for k in ("sd", "prep", "xpass", "ypass", "post") if name.replace("void ", "").replace("stereo::", "").startswith(k)), None)
     if not key:
         continue
     tot = 0.0
