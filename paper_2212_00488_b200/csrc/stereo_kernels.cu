@@ -799,9 +799,14 @@ __global__ void __launch_bounds__(kYThreads, 2)
       tma_load_3d(tile + st * 2 * TB * 16, tm, bar + st, x0, yt0, d + 2 * kYStages);
     }
     uint32_t o0 = upper ? b0 : 0u, o1 = upper ? b1 : 0u, oh = upper ? bh : 0u;
-    for (int q = 0; q < w; ++q) {
-      const uint4 t = tot[q * 16 + col];
-      o0 += t.x; o1 += t.y; oh += t.z;
+    // earlier warps' totals: unrolled, warp-uniform predicates, so that all
+    // loads issue back to back (one shared-memory latency, not w of them)
+#pragma unroll
+    for (int q = 0; q < kYThreads / 32 - 1; ++q) {
+      if (q < w) {
+        const uint4 t = tot[q * 16 + col];
+        o0 += t.x; o1 += t.y; oh += t.z;
+      }
     }
 #pragma unroll
     for (int s = 0; s < SEG; ++s) {
