@@ -317,13 +317,25 @@ def run_ours(args):
             alg = 2 * vol + 2 * n * 2 + 2 * n * 4  # write CA_x both bases; read pix + arms
         avg_ms = stage_ms[dom] / max(nfr, 1)
         achieved = alg / (avg_ms / 1e3) / 1e9
-        traffic = None
+        traffic, prof = None, {}
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(dom.lower())
+                prof = json.load(open(tp))
+                traffic = prof.get(dom.lower())
             except Exception:
-                traffic = None
+                traffic, prof = None, {}
+        pipes = prof.get("pipes", {})
+        # both aggregation kernels (north_star: "% HBM peak on the aggregation
+        # kernels" + their INT/ALU/LSU pipe use): algorithmic bytes / live
+        # single-stream kernel time, and the ncu pipe utilisation of one capture
+        algb = {"xpass": 2 * vol + 2 * n * 2 + 2 * n * 4, "ypass": 2 * vol + 2 * n * 4 + 2 * n}
+        aggregation = {}
+        for k in ("xpass", "ypass"):
+            us = stage_ms[k.upper()] / max(nfr, 1) * 1e3
+            gbs = algb[k] / (us / 1e6) / 1e9
+            aggregation[k] = {"us": us, "algorithmic_bytes": algb[k], "hbm_gbs": gbs,
+                              "hbm_frac": gbs / peak, "ncu_pipes": pipes.get(k)}
         step_ms = ms_max / args.steps
         line = {
             "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws, "steps": args.steps,
@@ -345,7 +357,8 @@ def run_ours(args):
             "roofline": {"kernel": dom.lower(), "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg},
+                         "algorithmic_bytes_per_launch": alg, "pipes": pipes.get(dom.lower())},
+            "aggregation_kernels": aggregation,
             "cpu_baseline": _cpu_baseline() if ws == 1 else None,
             "e2e": {"value": e2e_fps, "unit": "fps", "h2d_bytes_per_step": 2 * W * H,
                     "d2h_bytes_per_step": 4 * W * H, "steps": e2e_steps,

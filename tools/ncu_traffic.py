@@ -16,5 +16,23 @@ for r in rows[2:]:
         i = hdr.index(m)
         tot += float(r[i]) * scale[units[i]]
     out[key] = int(tot)
+    # pipe utilisation (the bound of the aggregation kernels is issue / shared
+    # memory, not HBM): percentages of peak over active cycles
+    def g(m):
+        try:
+            return float(r[hdr.index(m)])
+        except (ValueError, IndexError):
+            return None
+    cyc = g("sm__cycles_elapsed.avg") or None
+    wf = g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+    nsm = g("device__attribute_multiprocessor_count") or 148.0
+    out.setdefault("pipes", {})[key] = {
+        "issue_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "alu_pct": g("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+        "lsu_pct": g("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+        "smem_wavefronts_per_sm_cycle": (wf / nsm / cyc) if (wf and cyc) else None,
+        "bank_conflict_wavefronts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+        "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+    }
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
