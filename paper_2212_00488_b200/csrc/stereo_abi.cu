@@ -178,7 +178,8 @@ int enqueue_frame(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, c
     Ls = b.Ls;
     Rs = b.Rs;
   }
-  CU(launch_prep(g, h->plan, Ls, Rs, b, s));
+  const bool padded = (Ls == b.Ls && Rs == b.Rs) || (Ls == b.grayL && Rs == b.grayR);
+  CU(launch_prep(g, h->plan, Ls, Rs, padded, b, s));
   mark(STEREO_STAGE_PREP);
   CU(launch_xpass(g, h->plan, b, s));
   mark(STEREO_STAGE_XPASS);
@@ -293,7 +294,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       {(void**)&b.pixL, n * 2 + 16}, {(void**)&b.pixR, n * 2 + 16}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
       {(void**)&b.xrow, (size_t)4 * g.Hs * g.Wp * 4},
-      {(void**)&b.grayL, (size_t)W * H}, {(void**)&b.grayR, (size_t)W * H},
+      {(void**)&b.grayL, (size_t)W * H + 16}, {(void**)&b.grayR, (size_t)W * H + 16},
       {(void**)&b.DL, n + 16}, {(void**)&b.DR, n + 16}, {(void**)&b.masked, n}, {(void**)&b.median, n},
       {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
       {(void**)&b.patchVals, (size_t)g.Hs * 4},
@@ -304,7 +305,8 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
     if ((rc = alloc(h, a.p, a.bytes))) { stereo_destroy(h); return rc; }
   }
   if (g.K == 2) {
-    if ((rc = alloc(h, (void**)&b.Ls, n)) || (rc = alloc(h, (void**)&b.Rs, n))) {
+    // + 16: PREP reads these rows as unaligned words (3-byte over-read)
+    if ((rc = alloc(h, (void**)&b.Ls, n + 16)) || (rc = alloc(h, (void**)&b.Rs, n + 16))) {
       stereo_destroy(h);
       return rc;
     }
@@ -473,7 +475,7 @@ int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t*
       return STEREO_OK;
     case STEREO_STAGE_PREP:
       if (g.K == 1 && (!L || !R)) return fail(STEREO_EINVAL, "PREP with K=1 needs L and R");
-      CU(launch_prep(g, h->plan, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, b, s));
+      CU(launch_prep(g, h->plan, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, g.K == 2, b, s));
       return STEREO_OK;
     case STEREO_STAGE_XPASS: CU(launch_xpass(g, h->plan, b, s)); return STEREO_OK;
     case STEREO_STAGE_YPASS: CU(launch_ypass(g, h->plan, b, h->debug_ca, s)); return STEREO_OK;

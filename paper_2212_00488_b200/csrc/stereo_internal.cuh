@@ -83,7 +83,8 @@ struct Plan {
 // Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch error.
 cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const uint8_t* Rorg,
                       uint8_t* Ls, uint8_t* Rs, cudaStream_t s);
-cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
+// padded: Ls / Rs are handle buffers with >= 3 bytes of tail padding (word loads)
+cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs, bool padded,
                         Buffers& b, cudaStream_t s);
 cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s);
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,

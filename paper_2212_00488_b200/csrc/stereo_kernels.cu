@@ -83,16 +83,26 @@ cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const u
 // ============================================================================
 // PREP — mini-census (Fig. 3; pattern is a parameter, reading R8)
 // and the four cross arms (Steps 2 and 4)
-// of both scaled images.  A 32x32 pixel tile (4 rows per thread) is staged in shared memory as a
-// horizontal strip (rows +-2, cols +-max(w_x,2)) for the census and the x
-// arms and a TRANSPOSED vertical strip (cols +-2, rows +-max(w_y,2)) for the
-// y arms, so that both arm scans read contiguous bytes: 4 neighbours are
-// tested per step with byte-SIMD (|dI| via vabsdiffu4, >= delta via
-// vcmpgeu4), the run ends at the first dissimilar byte (ffs/clz).
-// Coordinates are clamped on load (census border rule R11); arm scans stop at
-// the real image border (R16).  Output: pix = I | code << 8 (u16),
-// arm = m | n<<8 | M<<16 | N<<24 (u32), and the x-pass rows (pitch Wp): code
-// word census | I << 24 and the x-window byte offsets 4(x-m) | 4(x+n+1) << 16.
+// of both scaled images.  Tile: 32 columns x TH rows, 8*TH threads, every
+// thread owning FOUR pixels so that the byte-SIMD video instructions work on
+// four pixels at once:
+//  * a horizontal strip (rows +-2, columns +-P4) serves the census and the
+//    x arms of the four consecutive pixels (x0+4g .. +3, y) of thread (y, g);
+//  * a TRANSPOSED vertical strip (column-major, rows +-Q4) serves the y arms of
+//    the four consecutive pixels (x, y0+4q .. +3) of thread (x, q);
+// census bit i of a pixel = [I(clamp(p + o_i)) < I(p)] (R9-R11; vcmpltu4 of
+// the four neighbour bytes at offset o_i against the four centre bytes).
+// An arm is the count of leading similar steps k = 1, 2, ...: per step one
+// funnel shift brings the four neighbour bytes at distance k, |dI| by
+// vabsdiffu4, the byte-SIMD ">= delta" test, an "alive" mask that stays 0
+// after the first dissimilar step (R15, R16) and a byte add.  Counts are
+// capped per pixel at min(w, distance to the image border) (R14, R16) with
+// one vminu4.  Coordinates are clamped on load (census border R11); source
+// rows are read as unaligned words (aligned pairs + funnel shift) when the
+// source is a handle buffer with tail padding, else bytewise.
+// Output: pix = I | code << 8 (u16), arm = m | n<<8 | M<<16 | N<<24 (u32),
+// and the x-pass rows (pitch Wp): code word census | I << 24 and the x-window
+// byte offsets 4(x-m) | 4(x+n+1) << 16.
 // ============================================================================
 struct PrepArgs {
   const uint8_t* img0;
@@ -103,7 +113,7 @@ struct PrepArgs {
   uint32_t* arm1;
   uint32_t* xrow;  // [4][Hs][Wp]: x-pass code L, R; window offsets L, R
   int Ws, Hs, Wp, w_x, w_x_r, w_y, delta;  // w_x: left image (D^L) x cap, w_x_r: right
-  int HX, HY, BWp, AHp;  // halos and padded strip pitches
+  int P4, BW, Q4, AV;  // strip pads and pitches in bytes (prep_geometry)
   int8_t cdx[6], cdy[6];
 };
 
@@ -115,113 +125,247 @@ __device__ __forceinline__ uint32_t dissimilar4(uint32_t diff, uint32_t dl4, boo
   const uint32_t lo = ((diff & 0x7f7f7f7fu) | 0x80808080u) - dl4;
   return (big ? (lo & diff) : (lo | diff)) & 0x80808080u;
 }
-// Length of the similar run starting at byte offset o (the first neighbour)
-// and going up, capped at lim: aligned 8-byte steps, first dissimilar byte by
-// ffs on the 64-bit mask.
-__device__ __forceinline__ int run_fwd(const uint32_t* s32, int o, int lim, uint32_t c4,
-                                       uint32_t dl4, bool big) {
-  int w = o >> 2, first = -(o & 3);
-  const uint64_t keep = ~0ull << (8 * (o & 3));  // ignore bytes before o
-  uint64_t m = ((uint64_t)dissimilar4(__vabsdiffu4(s32[w + 1], c4), dl4, big) << 32 |
-                dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big)) & keep;
-  for (;;) {
-    if (m) return min(first + ((__ffsll((long long)m) - 1) >> 3), lim);
-    first += 8;
-    if (first >= lim) return lim;
-    w += 2;
-    m = (uint64_t)dissimilar4(__vabsdiffu4(s32[w + 1], c4), dl4, big) << 32 |
-        dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big);
+
+// one step of four arm scans: `alive` keeps bit 7 of a pixel's byte while
+// every step so far was similar; cnt counts the similar steps per byte
+struct ArmStep {
+  uint32_t c4, dl4, alive, cnt;
+  bool big;
+  __device__ __forceinline__ void operator()(uint32_t nb4) {
+    alive &= ~dissimilar4(__vabsdiffu4(nb4, c4), dl4, big);
+    cnt += alive >> 7;
   }
+  __device__ __forceinline__ void sat(uint32_t nb4) {  // per-byte saturating count
+    alive &= ~dissimilar4(__vabsdiffu4(nb4, c4), dl4, big);
+    cnt = __vaddus4(cnt, alive >> 7);
+  }
+};
+
+// Leading similar steps k = 1 .. 4*ceil(kmax/4) of the four pixels whose
+// centre bytes are word cw of s, towards higher byte addresses (fwd) or lower
+// (bwd); per-byte counts, capped by the caller.  The loop bound is
+// warp-uniform; the warp stops once none of its pixels is still alive.
+// (Byte counts stay <= 252 in the loop; caps above 252, allowed up to 254,
+// take one more group with saturating adds.)
+__device__ __forceinline__ uint32_t arm4_fwd(const uint32_t* s, int cw, ArmStep st, int kmax) {
+  uint32_t lo = s[cw];
+  int q = 0;
+  for (; 4 * q < min(kmax, 252); ++q) {
+    const uint32_t hi = s[cw + q + 1];
+    st(__funnelshift_r(lo, hi, 8));
+    st(__funnelshift_r(lo, hi, 16));
+    st(__funnelshift_r(lo, hi, 24));
+    st(hi);
+    lo = hi;
+    if (!__any_sync(kFull, st.alive)) return st.cnt;
+  }
+  if (kmax > 252) {
+    const uint32_t hi = s[cw + q + 1];
+    st.sat(__funnelshift_r(lo, hi, 8));
+    st.sat(__funnelshift_r(lo, hi, 16));
+    st.sat(__funnelshift_r(lo, hi, 24));
+    st.sat(hi);
+  }
+  return st.cnt;
 }
-// Same going down from byte o - 1 (the first neighbour).
-__device__ __forceinline__ int run_bwd(const uint32_t* s32, int o, int lim, uint32_t c4,
-                                       uint32_t dl4, bool big) {
-  int w = (o - 1) >> 2, top = ((o - 1) & 3) + 4;  // distance of byte 0 of word w-1
-  const uint64_t keep = ~0ull >> (8 * (3 - ((o - 1) & 3)));  // ignore bytes above o-1
-  uint64_t m = ((uint64_t)dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) << 32 |
-                dissimilar4(__vabsdiffu4(s32[w - 1], c4), dl4, big)) & keep;
-  for (;;) {
-    if (m) return min(top - ((63 - __clzll((long long)m)) >> 3), lim);
-    top += 8;
-    if (top - 7 >= lim) return lim;
-    w -= 2;
-    m = (uint64_t)dissimilar4(__vabsdiffu4(s32[w], c4), dl4, big) << 32 |
-        dissimilar4(__vabsdiffu4(s32[w - 1], c4), dl4, big);
+__device__ __forceinline__ uint32_t arm4_bwd(const uint32_t* s, int cw, ArmStep st, int kmax) {
+  uint32_t hi = s[cw];
+  int q = 0;
+  for (; 4 * q < min(kmax, 252); ++q) {
+    const uint32_t lo = s[cw - q - 1];
+    st(__funnelshift_r(lo, hi, 24));
+    st(__funnelshift_r(lo, hi, 16));
+    st(__funnelshift_r(lo, hi, 8));
+    st(lo);
+    hi = lo;
+    if (!__any_sync(kFull, st.alive)) return st.cnt;
   }
+  if (kmax > 252) {
+    const uint32_t lo = s[cw - q - 1];
+    st.sat(__funnelshift_r(lo, hi, 24));
+    st.sat(__funnelshift_r(lo, hi, 16));
+    st.sat(__funnelshift_r(lo, hi, 8));
+    st.sat(lo);
+  }
+  return st.cnt;
 }
 
-// PR pixel rows per thread: tile 32 x 8PR pixels (taller tiles amortise the
-// vertical halo of the y-arm strip; the plan picks PR by grid size)
-template <int PR>
+// four bytes starting at p (any alignment): aligned word + successor (the
+// source buffer must allow a 3-byte over-read)
+__device__ __forceinline__ uint32_t ldg_u32_unaligned(const uint8_t* p) {
+  const uintptr_t ad = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~(uintptr_t)3);
+  const uint32_t lo = __ldg(w);
+  const int sh = 8 * (int)(ad & 3);
+  return sh ? __funnelshift_r(lo, __ldg(w + 1), sh) : lo;
+}
+
+// per-byte caps min(w, dist_i), dist_i = base + step * i (clamped at 0)
+__device__ __forceinline__ uint32_t caps4(int w, int base, int step) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c |= (uint32_t)max(0, min(w, base + step * i)) << (8 * i);
+  return c;
+}
+
+template <int TH, bool WORDS>
 __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
-  constexpr int kPrepRows = PR;
-  constexpr int kPrepTH = 8 * PR;       // tile height
-  constexpr int kPrepSB = kPrepTH + 4;  // rows of the horizontal strip
   extern __shared__ uint32_t psm32[];
-  uint8_t* sB = reinterpret_cast<uint8_t*>(psm32);  // [kPrepSB][BWp]  horizontal strip
-  uint8_t* sV = sB + kPrepSB * a.BWp;                 // [36][AHp]  vertical strip, transposed
+  const int BW = a.BW, AV = a.AV, P4 = a.P4, Q4 = a.Q4, Ws = a.Ws, Hs = a.Hs;
+  uint8_t* sB = reinterpret_cast<uint8_t*>(psm32);  // [TH+4][BW] horizontal strip
+  uint8_t* sV = sB + (TH + 4) * BW;                   // [32][AV]  vertical strip, column-major
+  uint8_t* sYM = sV + 32 * AV;                        // [TH][32]  M (up) of the tile pixels
+  uint8_t* sYN = sYM + TH * 32;                       // [TH][32]  N (down)
   const uint8_t* img = blockIdx.z ? a.img1 : a.img0;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * kPrepTH;
-  const int HX = a.HX, HY = a.HY, BWp = a.BWp, AHp = a.AHp;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int r = ty; r < kPrepSB; r += 8) {
-    const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, a.Hs - 1) * a.Ws;
-    for (int c = tx; c < BWp; c += 32) sB[r * BWp + c] = __ldg(row + clampi(x0 - HX - 8 + c, 0, a.Ws - 1));
-  }
-  // vertical strip, stored transposed (column-major, odd word pitch AHp/4 so
-  // the transposing byte stores of a warp hit distinct banks); loaded row by
-  // row: lane = column, the row pointer is computed once per row
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TH;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  constexpr int NW = TH / 4;  // warps
+
+  // ---- horizontal strip: rows y0-2 .. y0+TH+1, columns x0-P4 .. x0-P4+BW-1
   {
-    const int c0 = clampi(x0 - 2 + tx, 0, a.Ws - 1);
-    const int c1 = clampi(x0 + 30 + tx, 0, a.Ws - 1);  // columns 32..35 (tx < 4)
-    for (int r = ty; r < AHp; r += 8) {
-      const uint8_t* row = img + (size_t)clampi(y0 - HY - 8 + r, 0, a.Hs - 1) * a.Ws;
-      sV[tx * AHp + r] = __ldg(row + c0);
-      if (tx < 4) sV[(32 + tx) * AHp + r] = __ldg(row + c1);
+    const int cx0 = x0 - P4;
+    if (WORDS && cx0 >= 0 && cx0 + BW <= Ws) {
+      uint32_t* sB32 = reinterpret_cast<uint32_t*>(sB);
+      const int nwr = BW >> 2;
+      for (int r = warp; r < TH + 4; r += NW) {
+        const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, Hs - 1) * Ws + cx0;
+        for (int w = lane; w < nwr; w += 32) sB32[r * nwr + w] = ldg_u32_unaligned(row + 4 * w);
+      }
+    } else {
+      for (int r = warp; r < TH + 4; r += NW) {
+        const uint8_t* row = img + (size_t)clampi(y0 - 2 + r, 0, Hs - 1) * Ws;
+        for (int c = lane; c < BW; c += 32) sB[r * BW + c] = __ldg(row + clampi(cx0 + c, 0, Ws - 1));
+      }
+    }
+  }
+  // ---- vertical strip: tile column c at byte c*AV, strip row j = image row
+  // y0 - Q4 + j (clamped), j < TH + 2 Q4
+  {
+    const int nrow = TH + 2 * Q4;
+    if (WORDS && x0 + 32 <= Ws) {
+      // 4x4 byte blocks: four unaligned row words -> four column words
+      uint32_t* sV32 = reinterpret_cast<uint32_t*>(sV);
+      const int AVw = AV >> 2;
+      for (int i = t; i < (nrow >> 2) * 8; i += 8 * TH) {
+        const int jb = i >> 3, cb = i & 7;
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = ldg_u32_unaligned(img + (size_t)clampi(y0 - Q4 + 4 * jb + k, 0, Hs - 1) * Ws +
+                                   x0 + 4 * cb);
+        const uint32_t l01 = __byte_perm(w[0], w[1], 0x5140), h01 = __byte_perm(w[0], w[1], 0x7362);
+        const uint32_t l23 = __byte_perm(w[2], w[3], 0x5140), h23 = __byte_perm(w[2], w[3], 0x7362);
+        sV32[(4 * cb + 0) * AVw + jb] = __byte_perm(l01, l23, 0x5410);
+        sV32[(4 * cb + 1) * AVw + jb] = __byte_perm(l01, l23, 0x7632);
+        sV32[(4 * cb + 2) * AVw + jb] = __byte_perm(h01, h23, 0x5410);
+        sV32[(4 * cb + 3) * AVw + jb] = __byte_perm(h01, h23, 0x7632);
+      }
+    } else {
+      const int col = clampi(x0 + lane, 0, Ws - 1);
+      for (int j = warp; j < nrow; j += NW)
+        sV[lane * AV + j] = __ldg(img + (size_t)clampi(y0 - Q4 + j, 0, Hs - 1) * Ws + col);
     }
   }
   __syncthreads();
-  const int x = x0 + tx;
-  const size_t plane = (size_t)a.Hs * a.Wp;
+
   const bool big = a.delta >= 128;
   const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
+  const bool all_similar = a.delta > 255;  // |dI| <= 255 < delta: every step similar
   const int wx = blockIdx.z ? a.w_x_r : a.w_x;  // per-base x cap
-#pragma unroll 1
-  for (int rr = 0; rr < kPrepRows; ++rr) {
-    const int ty2 = ty + 8 * rr, y = y0 + ty2;
-    if (y >= a.Hs) return;
-    uint32_t* xr = a.xrow + blockIdx.z * plane + (size_t)y * a.Wp + x;
-    if (x >= a.Ws) {  // pitch padding of the x-pass rows: harmless windows, never read
-      if (x < a.Wp) {
-        xr[0] = 0u;
-        xr[2 * plane] = 4u * x | (4u * (x + 1)) << 16;
-      }
-      continue;
+
+  // ---- y arms: thread (column x0 + lane, rows y0 + 4 warp .. +3)
+  {
+    const uint32_t* colV = reinterpret_cast<const uint32_t*>(sV + lane * AV);
+    const int cwv = (Q4 >> 2) + warp;
+    const int yb = y0 + 4 * warp;
+    uint32_t N4 = 0xffffffffu, M4 = 0xffffffffu;
+    if (!all_similar) {
+      const ArmStep st{colV[cwv], dl4, 0x80808080u, 0u, big};
+      N4 = arm4_fwd(colV, cwv, st, a.w_y);
+      M4 = arm4_bwd(colV, cwv, st, a.w_y);
     }
-    const uint8_t* ctr = sB + (ty2 + 2) * BWp + tx + HX + 8;
-    const int c = *ctr;
-    int code = 0;
+    N4 = __vminu4(N4, caps4(a.w_y, Hs - 1 - yb, -1));
+    M4 = __vminu4(M4, caps4(a.w_y, yb, 1));
 #pragma unroll
-    for (int i = 0; i < 6; ++i) code |= (ctr[a.cdy[i] * BWp + a.cdx[i]] < c) << i;
-    int n, m, N, M;
-    if (a.delta > 255) {  // |dI| <= 255 < delta: every neighbour is similar
-      n = min(wx, a.Ws - 1 - x); m = min(wx, x);
-      N = min(a.w_y, a.Hs - 1 - y); M = min(a.w_y, y);
-    } else {
-      const uint32_t c4 = (uint32_t)c * 0x01010101u;
-      const int oB = (ty2 + 2) * BWp + tx + HX + 8;                      // centre in sB
-      const int oV = kPrepSB * BWp + (tx + 2) * AHp + ty2 + HY + 8;      // centre in sV
-      n = run_fwd(psm32, oB + 1, min(wx, a.Ws - 1 - x), c4, dl4, big);
-      m = run_bwd(psm32, oB, min(wx, x), c4, dl4, big);
-      N = run_fwd(psm32, oV + 1, min(a.w_y, a.Hs - 1 - y), c4, dl4, big);
-      M = run_bwd(psm32, oV, min(a.w_y, y), c4, dl4, big);
+    for (int i = 0; i < 4; ++i) {
+      sYN[(4 * warp + i) * 32 + lane] = (uint8_t)(N4 >> (8 * i));
+      sYM[(4 * warp + i) * 32 + lane] = (uint8_t)(M4 >> (8 * i));
     }
-    const size_t o = (size_t)y * a.Ws + x;
-    (blockIdx.z ? a.pix1 : a.pix0)[o] = (uint16_t)(c | (code << 8));
-    (blockIdx.z ? a.arm1 : a.arm0)[o] =
-        (uint32_t)m | ((uint32_t)n << 8) | ((uint32_t)M << 16) | ((uint32_t)N << 24);
-    xr[0] = (uint32_t)code | ((uint32_t)c << 24);
-    xr[2 * plane] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
+  }
+
+  // ---- census + x arms: thread (row y0 + r, pixels x0 + 4g .. +3)
+  const int r = t >> 3, g = t & 7;
+  const uint32_t* rowB = reinterpret_cast<const uint32_t*>(sB + (r + 2) * BW);
+  const int cw = (P4 >> 2) + g;
+  const uint32_t c4 = rowB[cw];
+  uint32_t code4 = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(sB + (r + 2 + a.cdy[i]) * BW);
+    const int bo = 4 * cw + a.cdx[i];
+    const int wi = bo >> 2, sh = 8 * (bo & 3);
+    const uint32_t nb4 = __funnelshift_r(rw[wi], rw[wi + 1], sh);
+    code4 |= (__vcmpltu4(nb4, c4) & 0x01010101u) << i;
+  }
+  const int xb = x0 + 4 * g;
+  uint32_t n4 = 0xffffffffu, m4 = 0xffffffffu;
+  if (!all_similar) {
+    const ArmStep st{c4, dl4, 0x80808080u, 0u, big};
+    n4 = arm4_fwd(rowB, cw, st, wx);
+    m4 = arm4_bwd(rowB, cw, st, wx);
+  }
+  n4 = __vminu4(n4, caps4(wx, Ws - 1 - xb, -1));
+  m4 = __vminu4(m4, caps4(wx, xb, 1));
+  __syncthreads();
+
+  // ---- outputs of the thread's four pixels
+  const int y = y0 + r;
+  if (y >= Hs) return;
+  const uint32_t M4 = *reinterpret_cast<const uint32_t*>(sYM + r * 32 + 4 * g);
+  const uint32_t N4 = *reinterpret_cast<const uint32_t*>(sYN + r * 32 + 4 * g);
+  const size_t plane = (size_t)Hs * a.Wp;
+  uint32_t* xr = a.xrow + blockIdx.z * plane + (size_t)y * a.Wp + xb;  // 16-B aligned (Wp = 32C)
+  const uint32_t mnl = __byte_perm(m4, n4, 0x5140), mnh = __byte_perm(m4, n4, 0x7362);
+  const uint32_t MNl = __byte_perm(M4, N4, 0x5140), MNh = __byte_perm(M4, N4, 0x7362);
+  const uint32_t armw[4] = {__byte_perm(mnl, MNl, 0x5410), __byte_perm(mnl, MNl, 0x7632),
+                            __byte_perm(mnh, MNh, 0x5410), __byte_perm(mnh, MNh, 0x7632)};
+  const uint32_t pixw[2] = {__byte_perm(c4, code4, 0x5140), __byte_perm(c4, code4, 0x7362)};
+  uint32_t codew[4], offw[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t x = (uint32_t)(xb + i);
+    codew[i] = ((code4 >> (8 * i)) & 0xffu) | ((c4 >> (8 * i)) << 24);
+    const uint32_t m = (m4 >> (8 * i)) & 0xffu, n = (n4 >> (8 * i)) & 0xffu;
+    offw[i] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
+  }
+  if (xb + 3 < Ws) {
+    uint16_t* pix = (blockIdx.z ? a.pix1 : a.pix0) + (size_t)y * Ws + xb;
+    uint32_t* arm = (blockIdx.z ? a.arm1 : a.arm0) + (size_t)y * Ws + xb;
+    *reinterpret_cast<uint4*>(xr) = make_uint4(codew[0], codew[1], codew[2], codew[3]);
+    *reinterpret_cast<uint4*>(xr + 2 * plane) = make_uint4(offw[0], offw[1], offw[2], offw[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) arm[i] = armw[i];
+    if ((reinterpret_cast<uintptr_t>(pix) & 3) == 0) {
+      reinterpret_cast<uint32_t*>(pix)[0] = pixw[0];
+      reinterpret_cast<uint32_t*>(pix)[1] = pixw[1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pix[i] = (uint16_t)(pixw[i >> 1] >> (16 * (i & 1)));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = xb + i;
+      if (x < Ws) {
+        xr[i] = codew[i];
+        xr[2 * plane + i] = offw[i];
+        (blockIdx.z ? a.arm1 : a.arm0)[(size_t)y * Ws + x] = armw[i];
+        (blockIdx.z ? a.pix1 : a.pix0)[(size_t)y * Ws + x] = (uint16_t)(pixw[i >> 1] >> (16 * (i & 1)));
+      } else if (x < a.Wp) {  // pitch padding of the x-pass rows: harmless windows, never read
+        xr[i] = 0u;
+        xr[2 * plane + i] = 4u * x | (4u * (x + 1)) << 16;
+      }
+    }
   }
 }
 
@@ -231,16 +375,26 @@ static int prep_rows_for(const Geom& g, int nsm) {
   return 1;
 }
 
-static void prep_geometry(const Geom& g, int pr, int& HX, int& HY, int& BWp, int& AHp) {
-  HX = g.w_x_max > 2 ? g.w_x_max : 2;
-  HY = g.w_y > 2 ? g.w_y : 2;
-  BWp = (32 + 2 * HX + 16 + 15) & ~15;
-  AHp = (8 * pr + 2 * HY + 16 + 3) & ~3;
-  if (((AHp >> 2) & 1) == 0) AHp += 4;  // odd word pitch: conflict-free transposed stores
+// Strip geometry (bytes): P4 / Q4 = pads, multiples of 4 covering the arm cap
+// rounded up to the 4-step granularity of the scans (and the census
+// footprint); BW = horizontal strip pitch with BW/4 = 8 or 24 (mod 32), so the
+// four rows a warp reads fall in distinct bank octets; AV = vertical strip
+// pitch with AV/4 odd (conflict-free column accesses).
+static void prep_geometry(const Geom& g, int th, int& P4, int& BW, int& Q4, int& AV) {
+  const int hx = g.w_x_max > 2 ? g.w_x_max : 2;
+  const int hy = g.w_y > 2 ? g.w_y : 2;
+  P4 = 4 * ((hx + 3) / 4) + 4;
+  BW = 32 + 2 * P4;
+  while ((BW / 4) % 32 != 8 && (BW / 4) % 32 != 24) BW += 4;
+  Q4 = 4 * ((hy + 3) / 4) + 4;
+  AV = th + 2 * Q4;
+  if (((AV >> 2) & 1) == 0) AV += 4;
 }
 
+static int prep_smem_bytes(int th, int BW, int AV) { return (th + 4) * BW + 32 * AV + 2 * th * 32 + 16; }
+
 cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
-                        Buffers& b, cudaStream_t s) {
+                        bool padded, Buffers& b, cudaStream_t s) {
   PrepArgs a;
   a.img0 = Ls; a.img1 = Rs;
   a.pix0 = b.pixL; a.pix1 = b.pixR;
@@ -248,13 +402,21 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
   a.xrow = b.xrow;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_x_r = g.w_x_r; a.w_y = g.w_y;
   a.delta = g.delta;
-  const int pr = p.prep_rows;
-  prep_geometry(g, pr, a.HX, a.HY, a.BWp, a.AHp);
+  const int th = 8 * p.prep_rows;
+  prep_geometry(g, th, a.P4, a.BW, a.Q4, a.AV);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
-  dim3 grid(g.Wp / 32, (g.Hs + 8 * pr - 1) / (8 * pr), 2);
-  if (pr == 4) prep_kernel<4><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
-  else if (pr == 2) prep_kernel<2><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
-  else prep_kernel<1><<<grid, dim3(32, 8), p.prep_smem, s>>>(a);
+  dim3 grid(g.Wp / 32, (g.Hs + th - 1) / th, 2);
+  const int smem = p.prep_smem;
+  if (th == 32) {
+    if (padded) prep_kernel<32, true><<<grid, 256, smem, s>>>(a);
+    else prep_kernel<32, false><<<grid, 256, smem, s>>>(a);
+  } else if (th == 16) {
+    if (padded) prep_kernel<16, true><<<grid, 128, smem, s>>>(a);
+    else prep_kernel<16, false><<<grid, 128, smem, s>>>(a);
+  } else {
+    if (padded) prep_kernel<8, true><<<grid, 64, smem, s>>>(a);
+    else prep_kernel<8, false><<<grid, 64, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -331,6 +493,35 @@ __device__ __forceinline__ void xpass_load_row(uint32_t* slot, uint64_t* bar, co
                : "memory");
   for (int k = 0; k < 4; ++k)
     bulk_g2s(slot + k * a.Wp, a.xrow + k * plane + (size_t)row * a.Wp, bytes, bar);
+}
+
+// Phase C of an item: CA_x of the lane's columns x = lane + 32 i for both
+// bases from the exclusive prefix rows (L: P_d, P_{d+1}; R: the same rows
+// shifted by d, resp. d + 1), one coalesced 128-B store per warp and output row.
+template <int C, bool TWO>
+__device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_t* sAR,
+                                              const char* P0, const char* P0d, const char* P1,
+                                              const char* P1d, uint32_t* outL, uint32_t* outR,
+                                              size_t dstep, int lane) {
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
+    const uint32_t alo = al & 0xffffu, ahi = al >> 16, arlo = ar & 0xffffu, arhi = ar >> 16;
+    const uint32_t caL = *reinterpret_cast<const uint32_t*>(P0 + ahi) -
+                         *reinterpret_cast<const uint32_t*>(P0 + alo);
+    const uint32_t caR = *reinterpret_cast<const uint32_t*>(P0d + arhi) -
+                         *reinterpret_cast<const uint32_t*>(P0d + arlo);
+    outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
+    outR[32 * i] = caR;
+    if (TWO) {
+      const uint32_t caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) -
+                            *reinterpret_cast<const uint32_t*>(P1 + alo);
+      const uint32_t caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) -
+                            *reinterpret_cast<const uint32_t*>(P1d + arlo);
+      outL[dstep + 32 * i] = caL1;
+      outR[dstep + 32 * i] = caR1;
+    }
+  }
 }
 
 template <int C, int ND>
@@ -445,27 +636,10 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp + lane;
     const size_t dstep = (size_t)a.Hs * a.Wp;
     const char* Pdb = Pb + 4 * d;
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
-      const uint32_t alo = al & 0xffffu, ahi = al >> 16, arlo = ar & 0xffffu, arhi = ar >> 16;
-      const uint32_t caL = *reinterpret_cast<const uint32_t*>(Pb + ahi) -
-                           *reinterpret_cast<const uint32_t*>(Pb + alo);
-      const uint32_t caR = *reinterpret_cast<const uint32_t*>(Pdb + arhi) -
-                           *reinterpret_cast<const uint32_t*>(Pdb + arlo);
-      outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
-      outR[32 * i] = caR;
-      if (ND == 2 && two) {
-        const char* P1 = Pb + PLb;
-        const char* P1d = Pdb + PLb + 4;
-        const uint32_t caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) -
-                              *reinterpret_cast<const uint32_t*>(P1 + alo);
-        const uint32_t caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) -
-                              *reinterpret_cast<const uint32_t*>(P1d + arlo);
-        outL[dstep + 32 * i] = caL1;
-        outR[dstep + 32 * i] = caR1;
-      }
-    }
+    if (ND == 2 && two)  // (the single-disparity tail item exists only for odd Ds)
+      xpass_windows<C, true>(sAL, sAR, Pb, Pdb, Pb + PLb, Pdb + PLb + 4, outL, outR, dstep, lane);
+    else
+      xpass_windows<C, false>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, dstep, lane);
     __syncwarp();
     // ---- release the row slot: the warp finishing the row's last item of
     // this range refills the slot with the row `slots` ahead
@@ -1285,7 +1459,8 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   const int R = p.post_rows, nt = p.post_threads;
   if (R == 1) post_kernel<1><<<g.Hs, nt, p.post_smem, s>>>(a);
   else if (R == 2) post_kernel<2><<<(g.Hs + 1) / 2, nt, p.post_smem, s>>>(a);
-  else post_kernel<4><<<(g.Hs + 3) / 4, nt, p.post_smem, s>>>(a);
+  else if (R == 4) post_kernel<4><<<(g.Hs + 3) / 4, nt, p.post_smem, s>>>(a);
+  else post_kernel<8><<<(g.Hs + 7) / 8, nt, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1378,23 +1553,34 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   // SD / PREP / POST dynamic shared memory
   p.sd_smem = (2 * g.m_pool + 1) * ((g.W + 3) & ~3) + 16;
   {
-    int HX, HY, BWp, AHp;
-    p.prep_rows = prep_rows_for(g, nsm);
-    prep_geometry(g, p.prep_rows, HX, HY, BWp, AHp);
-    p.prep_smem = (8 * p.prep_rows + 4) * BWp + 36 * AHp + 16;
+    p.prep_rows = env_int("STEREO_PREP_ROWS", prep_rows_for(g, nsm), 1, 4);
+    if (p.prep_rows == 3) p.prep_rows = 2;
+    int P4, BW, Q4, AV;
+    prep_geometry(g, 8 * p.prep_rows, P4, BW, Q4, AV);
+    p.prep_smem = prep_smem_bytes(8 * p.prep_rows, BW, AV);
   }
   const int Wsp = (g.Ws + 31) & ~31;
   const int Wx = (g.W + 3) & ~3;
   // 2 rows x 512 threads per CTA: measured best at c2/c3 among {1,2,4} x {256,512}
-  p.post_rows = 2;
-  p.post_threads = 512;
+  p.post_rows = env_int("STEREO_POST_ROWS", 2, 1, 8);
+  if (p.post_rows == 3) p.post_rows = 2;
+  if (p.post_rows > 4) p.post_rows = 8;
+  p.post_threads = env_int("STEREO_POST_THREADS", 512, 128, 512) & ~127;
+  // step 4 of POST runs one warp per fill row (R + 1 of them)
+  p.post_threads = std::max(p.post_threads, (32 * (p.post_rows + 1) + 127) & ~127);
   {
     const int R = p.post_rows;
     p.post_smem = (R + 3) * Wsp + (R + 1) * Wsp + (R + 1) * Wsp * 4 + (R + 1) * Wx * 4 +
                   3 * (R + 1) * 64 * 4 + (R + 1) * Wsp * 2 + 2 * (R + 3) * Wsp + (R + 1) * Wx + 64;
   }
+  if (p.prep_smem > 48 * 1024) {
+    for (auto fn : {prep_kernel<32, true>, prep_kernel<32, false>, prep_kernel<16, true>,
+                    prep_kernel<16, false>, prep_kernel<8, true>, prep_kernel<8, false>})
+      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.prep_smem)))
+        return e;
+  }
   if (p.post_smem > 48 * 1024) {
-    for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>})
+    for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>, post_kernel<8>})
       if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
         return e;
   }

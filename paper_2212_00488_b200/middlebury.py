@@ -128,7 +128,7 @@ def _load_rgb(path) -> np.ndarray:
     im = Image.open(path)
     if im.mode not in ("RGB", "L", "RGBA"):
         raise ValueError(f"{path}: unsupported image mode {im.mode}")
-    return np.ascontiguousarray(np.asarray(im.convert("RGB"), dtype=np.uint8))
+    return np.array(im.convert("RGB"), dtype=np.uint8)  # writable copy
 
 
 def run_scene(scene_dir: str, threshold: float = 2.0, k_scale: int = 2, **params) -> EvalReport:

@@ -31,11 +31,17 @@ def run(cfg, nstreams, n=600):
     outs = [torch.empty((H, W), dtype=torch.float32, device="cuda") for _ in range(nstreams)]
     info = hs[0].info
 
+    stages = [int(v) for v in os.environ.get("TP_STAGES", "").split(",") if v]
+
     def go(m):
         for i in range(m):
             j = i % nstreams
             with torch.cuda.stream(ss[j]):
-                hs[j].compute(Ls[i % POOL], Rs[i % POOL], outs[j])
+                if stages and i >= nstreams:  # subset of stages on the buffers of a full frame
+                    for sid in stages:
+                        hs[j].run_stage(sid, Ls[i % POOL], Rs[i % POOL], outs[j], stream=ss[j])
+                else:
+                    hs[j].compute(Ls[i % POOL], Rs[i % POOL], outs[j])
 
     go(60)
     torch.cuda.synchronize()
