@@ -117,26 +117,28 @@ struct PrepArgs {
   int8_t cdx[6], cdy[6];
 };
 
-// Byte-SIMD "dissimilar" test: bit 7 of byte i of the result is set iff byte
-// i of `diff` (an |dI|) is >= delta, for 1 <= delta <= 255.  dl4 replicates
-// delta (delta < 128) or delta - 128 (delta >= 128, `big`).  Three ALU ops:
-// ((diff & 0x7f) | 0x80) - dl never borrows across bytes.
-__device__ __forceinline__ uint32_t dissimilar4(uint32_t diff, uint32_t dl4, bool big) {
-  const uint32_t lo = ((diff & 0x7f7f7f7fu) | 0x80808080u) - dl4;
-  return (big ? (lo & diff) : (lo | diff)) & 0x80808080u;
-}
-
 // one step of four arm scans: `alive` keeps bit 7 of a pixel's byte while
-// every step so far was similar; cnt counts the similar steps per byte
+// every step so far was similar; cnt counts the similar steps per byte.
+// The ">= delta" test on |dI| bytes (1 <= delta <= 255): dl4 replicates
+// delta (delta < 128) or delta - 128 (BIG, delta >= 128);
+// lo = ((diff & 0x7f) | 0x80) - dl never borrows across bytes, and bit 7 of
+// (BIG ? lo & diff : lo | diff) is set iff diff >= delta.  BIG is a template
+// parameter so that the test and the alive update fold into one three-input
+// logic op (alive carries bit 7 only: no final mask).
+template <bool BIG>
 struct ArmStep {
   uint32_t c4, dl4, alive, cnt;
-  bool big;
+  __device__ __forceinline__ uint32_t kill(uint32_t nb4) const {  // bit 7: dissimilar
+    const uint32_t diff = __vabsdiffu4(nb4, c4);
+    const uint32_t lo = ((diff & 0x7f7f7f7fu) | 0x80808080u) - dl4;
+    return BIG ? (lo & diff) : (lo | diff);
+  }
   __device__ __forceinline__ void operator()(uint32_t nb4) {
-    alive &= ~dissimilar4(__vabsdiffu4(nb4, c4), dl4, big);
+    alive &= ~kill(nb4);
     cnt += alive >> 7;
   }
   __device__ __forceinline__ void sat(uint32_t nb4) {  // per-byte saturating count
-    alive &= ~dissimilar4(__vabsdiffu4(nb4, c4), dl4, big);
+    alive &= ~kill(nb4);
     cnt = __vaddus4(cnt, alive >> 7);
   }
 };
@@ -147,7 +149,8 @@ struct ArmStep {
 // warp-uniform; the warp stops once none of its pixels is still alive.
 // (Byte counts stay <= 252 in the loop; caps above 252, allowed up to 254,
 // take one more group with saturating adds.)
-__device__ __forceinline__ uint32_t arm4_fwd(const uint32_t* s, int cw, ArmStep st, int kmax) {
+template <bool BIG>
+__device__ __forceinline__ uint32_t arm4_fwd(const uint32_t* s, int cw, ArmStep<BIG> st, int kmax) {
   uint32_t lo = s[cw];
   int q = 0;
   for (; 4 * q < min(kmax, 252); ++q) {
@@ -168,7 +171,8 @@ __device__ __forceinline__ uint32_t arm4_fwd(const uint32_t* s, int cw, ArmStep 
   }
   return st.cnt;
 }
-__device__ __forceinline__ uint32_t arm4_bwd(const uint32_t* s, int cw, ArmStep st, int kmax) {
+template <bool BIG>
+__device__ __forceinline__ uint32_t arm4_bwd(const uint32_t* s, int cw, ArmStep<BIG> st, int kmax) {
   uint32_t hi = s[cw];
   int q = 0;
   for (; 4 * q < min(kmax, 252); ++q) {
@@ -188,6 +192,22 @@ __device__ __forceinline__ uint32_t arm4_bwd(const uint32_t* s, int cw, ArmStep 
     st.sat(lo);
   }
   return st.cnt;
+}
+
+// both arms of the four pixels at word cw of s (fwd -> f, bwd -> b)
+__device__ __forceinline__ void arms4(const uint32_t* s, int cw, uint32_t dl4, int delta, int kmax,
+                                      uint32_t& f, uint32_t& b) {
+  if (delta > 255) {  // |dI| <= 255 < delta: every step similar, the caps decide
+    f = b = 0xffffffffu;
+  } else if (delta >= 128) {
+    const ArmStep<true> st{s[cw], dl4, 0x80808080u, 0u};
+    f = arm4_fwd(s, cw, st, kmax);
+    b = arm4_bwd(s, cw, st, kmax);
+  } else {
+    const ArmStep<false> st{s[cw], dl4, 0x80808080u, 0u};
+    f = arm4_fwd(s, cw, st, kmax);
+    b = arm4_bwd(s, cw, st, kmax);
+  }
 }
 
 // four bytes starting at p (any alignment): aligned word + successor (the
@@ -268,9 +288,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   }
   __syncthreads();
 
-  const bool big = a.delta >= 128;
-  const uint32_t dl4 = (uint32_t)(big ? a.delta - 128 : a.delta) * 0x01010101u;
-  const bool all_similar = a.delta > 255;  // |dI| <= 255 < delta: every step similar
+  const uint32_t dl4 = (uint32_t)(a.delta >= 128 ? a.delta - 128 : a.delta) * 0x01010101u;
   const int wx = blockIdx.z ? a.w_x_r : a.w_x;  // per-base x cap
 
   // ---- y arms: thread (column x0 + lane, rows y0 + 4 warp .. +3)
@@ -278,12 +296,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     const uint32_t* colV = reinterpret_cast<const uint32_t*>(sV + lane * AV);
     const int cwv = (Q4 >> 2) + warp;
     const int yb = y0 + 4 * warp;
-    uint32_t N4 = 0xffffffffu, M4 = 0xffffffffu;
-    if (!all_similar) {
-      const ArmStep st{colV[cwv], dl4, 0x80808080u, 0u, big};
-      N4 = arm4_fwd(colV, cwv, st, a.w_y);
-      M4 = arm4_bwd(colV, cwv, st, a.w_y);
-    }
+    uint32_t N4, M4;
+    arms4(colV, cwv, dl4, a.delta, a.w_y, N4, M4);
     N4 = __vminu4(N4, caps4(a.w_y, Hs - 1 - yb, -1));
     M4 = __vminu4(M4, caps4(a.w_y, yb, 1));
 #pragma unroll
@@ -308,12 +322,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     code4 |= (__vcmpltu4(nb4, c4) & 0x01010101u) << i;
   }
   const int xb = x0 + 4 * g;
-  uint32_t n4 = 0xffffffffu, m4 = 0xffffffffu;
-  if (!all_similar) {
-    const ArmStep st{c4, dl4, 0x80808080u, 0u, big};
-    n4 = arm4_fwd(rowB, cw, st, wx);
-    m4 = arm4_bwd(rowB, cw, st, wx);
-  }
+  uint32_t n4, m4;
+  arms4(rowB, cw, dl4, a.delta, wx, n4, m4);
   n4 = __vminu4(n4, caps4(wx, Ws - 1 - xb, -1));
   m4 = __vminu4(m4, caps4(wx, xb, 1));
   __syncthreads();
@@ -1200,24 +1210,29 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   const int nf = a.K == 2 ? min(nr + 1, a.Hs - y0) : nr;     // fill rows needed (SU reads y+1)
   const float thr = (float)(a.K * a.T);
 
-  // 0. stage every input row in shared memory: one batch of independent
-  // word loads (rows are re-aligned with a funnel shift; the handle's own
-  // buffers carry 16 bytes of tail padding for the over-read)
-  for (int r = 0; r < nf + 2; ++r) {
-    const size_t o = (size_t)clampi(y0 - 1 + r, 0, a.Hs - 1) * Ws;
-    stage_row(sDL + r * Wsp, a.DL + o, Ws, tid, blockDim.x);
-    stage_row(sDR + r * Wsp, a.DR + o, Ws, tid, blockDim.x);
-  }
-  for (int j = 0; j < nf; ++j) {
-    stage_row(reinterpret_cast<uint8_t*>(sPix + j * Wsp),
-              reinterpret_cast<const uint8_t*>(a.pixL + (size_t)(y0 + j) * Ws), 2 * Ws, tid,
-              blockDim.x);
-    if (a.K == 2) {
-      const uint8_t* src = a.Lorg + (size_t)(2 * (y0 + j)) * W;
-      if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)W) & 3) == 0) {  // caller buffer:
-        stage_row(sLo + j * Wx, src, W, tid, blockDim.x);                // no over-read
+  // 0. stage every input row in shared memory, one warp per row (rows are
+  // re-aligned with a funnel shift; the handle's own buffers carry 16 bytes
+  // of tail padding for the over-read): D^L, D^R rows y0-1 .. y0+nf (clamped),
+  // pix rows y0 .. y0+nf-1, L_org rows 2(y0+j) (K = 2)
+  {
+    const int nwarp = blockDim.x >> 5;
+    const int nmap = nf + 2, nrows = 2 * nmap + nf + (a.K == 2 ? nf : 0);
+    for (int q = warp; q < nrows; q += nwarp) {
+      if (q < 2 * nmap) {
+        const int r = q < nmap ? q : q - nmap;
+        const size_t o = (size_t)clampi(y0 - 1 + r, 0, a.Hs - 1) * Ws;
+        stage_row(q < nmap ? sDL + r * Wsp : sDR + r * Wsp, (q < nmap ? a.DL : a.DR) + o, Ws, lane, 32);
+      } else if (q < 2 * nmap + nf) {
+        const int j = q - 2 * nmap;
+        stage_row(reinterpret_cast<uint8_t*>(sPix + j * Wsp),
+                  reinterpret_cast<const uint8_t*>(a.pixL + (size_t)(y0 + j) * Ws), 2 * Ws, lane, 32);
       } else {
-        for (int X = tid; X < W; X += blockDim.x) sLo[j * Wx + X] = __ldg(src + X);
+        const int j = q - 2 * nmap - nf;
+        const uint8_t* src = a.Lorg + (size_t)(2 * (y0 + j)) * W;
+        if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)W) & 3) == 0)  // caller buffer:
+          stage_row(sLo + j * Wx, src, W, lane, 32);                       // no over-read
+        else
+          for (int X = lane; X < W; X += 32) sLo[j * Wx + X] = __ldg(src + X);
       }
     }
   }
