@@ -1073,6 +1073,10 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
 // Rows without any valid pixel (rule (d)) are patched by the last CTA to
 // finish (grid-wide counter), which sees every row's first/last valid column.
 // ============================================================================
+// POST row pitch in shared memory: room for the clamp byte at Ws and the
+// word over-reads of the SIMD median, a multiple of 32 (ballot chunks)
+static int post_pitch(int Ws) { return (Ws + 8 + 31) & ~31; }
+
 struct PostArgs {
   const uint8_t* DL;
   const uint8_t* DR;
@@ -1087,7 +1091,7 @@ struct PostArgs {
   unsigned* counter;
   int W, H, Ws, Hs, K, T;
   int fill_mode;  // STEREO_FILL_*
-  int Wsp;  // Ws rounded up to 32
+  int Wsp;  // smem row pitch, post_pitch(Ws)
   int Wx;   // W rounded up to 4
 };
 
@@ -1095,6 +1099,29 @@ __device__ __forceinline__ void cswap(int& a, int& b) {
   const int lo = min(a, b), hi = max(a, b);
   a = lo;
   b = hi;
+}
+
+// u16x2 helpers of the SIMD median (lanes hold values 0..255, INVALID = 255)
+__device__ __forceinline__ void cswap16(uint32_t& a, uint32_t& b) {
+  const uint32_t lo = __vminu2(a, b), hi = __vmaxu2(a, b);
+  a = lo;
+  b = hi;
+}
+// 0xffff in the lanes of w equal to 255 (bit 15 of w + 0x7f01, replicated)
+// (prmt sign-replicate mode via PTX: __byte_perm keeps only 3 selector bits)
+__device__ __forceinline__ uint32_t inv16(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(r) : "r"(w + 0x7f017f01u));
+  return r;
+}
+// per lane: key valid (< 255) ? val : cur
+__device__ __forceinline__ uint32_t sel16_valid(uint32_t key, uint32_t val, uint32_t cur) {
+  const uint32_t m = inv16(key);
+  return (cur & m) | (val & ~m);
+}
+// bytes 2h, 2h+1 of w as u16x2 lanes
+__device__ __forceinline__ uint32_t u16x2_of(uint32_t w, int h) {
+  return h ? __byte_perm(w, 0, 0x4342) : __byte_perm(w, 0, 0x4140);
 }
 
 // Step8 x rule on seeded row `f` (fill values) with original-resolution row `L`
@@ -1237,45 +1264,80 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
     }
   }
   __syncthreads();
-  // 1. masked rows y0-1 .. y0+nf (clamped), Eq. 10
+  // 1. masked rows y0-1 .. y0+nf (clamped), Eq. 10; four pixels per thread.
+  // Byte Ws of every row repeats byte Ws-1 (the clamped right neighbour of
+  // the median below).
+  const int nq = (Ws + 3) >> 2;
   for (int r = 0; r < nf + 2; ++r)
-    for (int x = tid; x < Ws; x += blockDim.x) {
-      const int k = sDL[r * Wsp + x];
-      const bool gcp = (x - k >= 0) && (sDR[r * Wsp + x - k] == k);
-      mk[r * Wsp + x] = gcp ? (uint8_t)k : (uint8_t)kInvalid;
+    for (int q = tid; q < nq; q += blockDim.x) {
+      const int x = 4 * q;
+      const uint32_t k4 = *reinterpret_cast<const uint32_t*>(sDL + r * Wsp + x);
+      const uint8_t* dr = sDR + r * Wsp;
+      uint32_t m4 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = (k4 >> (8 * i)) & 255;
+        const bool gcp = (x + i - k >= 0) && (dr[max(x + i - k, 0)] == k);
+        m4 |= (uint32_t)(gcp ? k : kInvalid) << (8 * i);
+      }
+      *reinterpret_cast<uint32_t*>(mk + r * Wsp + x) = m4;
+      if (x + 4 >= Ws) mk[r * Wsp + Ws] = mk[r * Wsp + Ws - 1];  // (this thread wrote Ws-1)
     }
   __syncthreads();
-  // 2. median rows y0 .. y0+nf-1
+  // 2. median rows y0 .. y0+nf-1: the 25-comparator 9-sorting network on two
+  // pixels at a time (u16x2 lanes, native VIMNMX.U16x2), four pixels per
+  // thread.  INVALID (255) sorts last, so with n valid neighbours the median
+  // sorted[(n-1)/2] is s0, then s1 if s2 is valid, s2 if s4 is, s3 if s6 is,
+  // s4 if s8 is (R21-R23); an INVALID centre stays INVALID.
   for (int j = 0; j < nf; ++j) {
-    const uint8_t* r0 = mk + j * Wsp;
-    const uint8_t* r1 = r0 + Wsp;
-    const uint8_t* r2 = r1 + Wsp;
-    for (int x = tid; x < Ws; x += blockDim.x) {
-      const int c = r1[x];
-      int out = kInvalid;
-      if (c != kInvalid) {
-        const int xl = max(x - 1, 0), xr_ = min(x + 1, Ws - 1);
-        int v0 = r0[xl], v1 = r0[x], v2 = r0[xr_];
-        int v3 = r1[xl], v4 = c, v5 = r1[xr_];
-        int v6 = r2[xl], v7 = r2[x], v8 = r2[xr_];
-        const int n = (v0 != kInvalid) + (v1 != kInvalid) + (v2 != kInvalid) + (v3 != kInvalid) +
-                      1 + (v5 != kInvalid) + (v6 != kInvalid) + (v7 != kInvalid) + (v8 != kInvalid);
-        cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
-        cswap(v1, v2); cswap(v4, v5); cswap(v7, v8);
-        cswap(v0, v1); cswap(v3, v4); cswap(v6, v7);
-        cswap(v0, v3); cswap(v3, v6); cswap(v0, v3);
-        cswap(v1, v4); cswap(v4, v7); cswap(v1, v4);
-        cswap(v2, v5); cswap(v5, v8); cswap(v2, v5);
-        cswap(v1, v3); cswap(v5, v7); cswap(v2, v6);
-        cswap(v4, v6); cswap(v2, v4); cswap(v2, v3);
-        cswap(v5, v6);
-        const int kk = (n - 1) >> 1;  // 0..4
-        out = kk == 0 ? v0 : kk == 1 ? v1 : kk == 2 ? v2 : kk == 3 ? v3 : v4;
+    for (int q = tid; q < nq; q += blockDim.x) {
+      const int x = 4 * q;
+      uint32_t v[2][9];
+      uint32_t cword = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(mk + (j + k) * Wsp + x);
+        const uint32_t wb = w[0], wc = w[1];
+        // bytes x-1 .. x+2 (x-1 clamped to x at the left border) and x+1 .. x+4
+        const uint32_t W0 = x ? __funnelshift_r(w[-1], wb, 24) : __byte_perm(wb, 0, 0x2100);
+        const uint32_t W1 = __funnelshift_r(wb, wc, 8);
+        v[0][3 * k + 0] = __byte_perm(W0, 0, 0x4140);  // (x-1, x)
+        v[0][3 * k + 1] = __byte_perm(W0, 0, 0x4241);  // (x, x+1)
+        v[0][3 * k + 2] = __byte_perm(W0, 0, 0x4342);  // (x+1, x+2)
+        v[1][3 * k + 0] = __byte_perm(W1, 0, 0x4140);  // (x+1, x+2)
+        v[1][3 * k + 1] = __byte_perm(W1, 0, 0x4241);  // (x+2, x+3)
+        v[1][3 * k + 2] = __byte_perm(W1, 0, 0x4342);  // (x+3, x+4)
+        if (k == 1) cword = wb;
       }
-      md[j * Wsp + x] = (uint8_t)out;
+      uint32_t out[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t* u = v[h];
+        cswap16(u[0], u[1]); cswap16(u[3], u[4]); cswap16(u[6], u[7]);
+        cswap16(u[1], u[2]); cswap16(u[4], u[5]); cswap16(u[7], u[8]);
+        cswap16(u[0], u[1]); cswap16(u[3], u[4]); cswap16(u[6], u[7]);
+        cswap16(u[0], u[3]); cswap16(u[3], u[6]); cswap16(u[0], u[3]);
+        cswap16(u[1], u[4]); cswap16(u[4], u[7]); cswap16(u[1], u[4]);
+        cswap16(u[2], u[5]); cswap16(u[5], u[8]); cswap16(u[2], u[5]);
+        cswap16(u[1], u[3]); cswap16(u[5], u[7]); cswap16(u[2], u[6]);
+        cswap16(u[4], u[6]); cswap16(u[2], u[4]); cswap16(u[2], u[3]);
+        cswap16(u[5], u[6]);
+        uint32_t med = u[0];
+        med = sel16_valid(u[2], u[1], med);
+        med = sel16_valid(u[4], u[2], med);
+        med = sel16_valid(u[6], u[3], med);
+        med = sel16_valid(u[8], u[4], med);
+        out[h] = med | inv16(u16x2_of(cword, h));  // INVALID centre stays INVALID
+      }
+      const uint32_t o4 = __byte_perm(out[0], out[1], 0x6420);
+      *reinterpret_cast<uint32_t*>(md + j * Wsp + x) = o4;
       if (j < nr) {
-        a.masked[(size_t)(y0 + j) * Ws + x] = (uint8_t)c;
-        a.median[(size_t)(y0 + j) * Ws + x] = (uint8_t)out;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (x + i < Ws) {
+            a.masked[(size_t)(y0 + j) * Ws + x + i] = (uint8_t)(cword >> (8 * i));
+            a.median[(size_t)(y0 + j) * Ws + x + i] = (uint8_t)(o4 >> (8 * i));
+          }
       }
     }
   }
@@ -1455,7 +1517,7 @@ cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* 
   a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.fill_mode = g.fill_mode;
-  a.Wsp = (g.Ws + 31) & ~31;
+  a.Wsp = post_pitch(g.Ws);
   a.Wx = (g.W + 3) & ~3;
   patch_kernel<<<1, 256, 0, s>>>(a, rows_dev, vals_dev, n);
   return cudaGetLastError();
@@ -1469,7 +1531,7 @@ cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t*
   a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.fill_mode = g.fill_mode;
-  a.Wsp = (g.Ws + 31) & ~31;
+  a.Wsp = post_pitch(g.Ws);
   a.Wx = (g.W + 3) & ~3;
   const int R = p.post_rows, nt = p.post_threads;
   if (R == 1) post_kernel<1><<<g.Hs, nt, p.post_smem, s>>>(a);
@@ -1574,7 +1636,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     prep_geometry(g, 8 * p.prep_rows, P4, BW, Q4, AV);
     p.prep_smem = prep_smem_bytes(8 * p.prep_rows, BW, AV);
   }
-  const int Wsp = (g.Ws + 31) & ~31;
+  const int Wsp = post_pitch(g.Ws);
   const int Wx = (g.W + 3) & ~3;
   // 2 rows x 512 threads per CTA: measured best at c2/c3 among {1,2,4} x {256,512}
   p.post_rows = env_int("STEREO_POST_ROWS", 2, 1, 8);
