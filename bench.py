@@ -205,10 +205,18 @@ def run_ours(args):
     ws, rank, local = _dist()
     if ws != args.gpus:
         print(f"warning: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
+    # STEREO_BENCH_BACKEND=gloo (test only): run N > 1 ranks on fewer GPUs to
+    # exercise the multi-rank path; the product run is NCCL, one rank per GPU
+    backend = os.environ.get("STEREO_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    rdev = torch.device("cpu") if backend == "gloo" else dev  # device of the reduced scalars
     NS = max(1, args.streams)
     handles = [abi.Stereo(W, H, D) for _ in range(NS)]  # one handle per stream (not re-entrant)
     st = handles[0]
@@ -263,7 +271,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     stage_ms, nfr = st.stage_times_ms()
     st.set_timing(False)
-    t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms_total], device=rdev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -298,7 +306,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     e2e_ms = max(ea[i].elapsed_time(eb[j]) for i in range(NE) for j in range(NE))
-    t2 = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    t2 = torch.tensor([e2e_ms], device=rdev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_fps = ws * e2e_steps / (float(t2.item()) / 1e3)
