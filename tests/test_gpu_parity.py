@@ -146,6 +146,31 @@ def test_edge_shapes(W, H, D, K):
     _compare(L, R, D, dict(k_scale=K))
 
 
+@pytest.mark.parametrize("delta", [127, 128, 129, 200, 255, 256, 1000])
+@pytest.mark.parametrize("K", [1, 2])
+def test_prep_delta_extremes(delta, K):
+    """PREP's byte-SIMD similarity test across its cases: delta < 128, the
+    delta >= 128 template, delta = 255 and delta > 255 (every neighbour
+    similar, arms = caps); noise at 256 levels and a scene."""
+    L, R = synth.random_pair(97, 61, seed=delta + K, levels=256)
+    _compare(L, R, 12, dict(k_scale=K, delta=delta))
+    L, R, _ = synth.scene(130, 70, 20, seed=delta)
+    _compare(L, R, 20, dict(k_scale=K, delta=delta, w_x=40, w_y=25))
+
+
+@pytest.mark.parametrize("w_x,w_y", [(254, 112), (253, 3), (252, 0), (0, 112)])
+def test_prep_arm_caps_extremes(w_x, w_y):
+    """Arm caps at the top of the u8 range (the saturating tail group of the
+    byte-SIMD scans beyond 252 steps) on flat rows that let the arms reach
+    them; K = 1 so that 300 columns stay 300."""
+    rng = np.random.default_rng(w_x + w_y)
+    L = np.full((24, 300), 90, np.uint8)
+    L[:, 150:] = 160                     # one step edge: arms stop there
+    L[5] = rng.integers(0, 256, 300)     # a textured row
+    R = np.roll(L, 3, axis=1)
+    _compare(L, R, 6, dict(k_scale=1, w_x=w_x, w_y=w_y, delta=20))
+
+
 def test_c2_quarter_scene_bit_exact():
     L, R, _ = synth.scene(450, 375, 64, seed=1)
     _compare(L, R, 64, dict(k_scale=1))
