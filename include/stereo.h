@@ -90,7 +90,7 @@ typedef struct {
   int32_t frac_bits;      /* f of the fixed-point cost */
   int32_t device;         /* CUDA device ordinal the handle is bound to */
   uint64_t device_bytes;  /* total device scratch owned by the handle */
-  uint64_t cax_bytes;     /* bytes of ONE CA_x volume (u32 [Ds][Hs][cax_pitch]) */
+  uint64_t cax_bytes;     /* bytes of ONE CA_x volume (u32 [ceil(Ds/2)][Hs][cax_pitch][2]) */
   int32_t launches_per_frame; /* kernels enqueued by one stereo_compute */
   int32_t ypass_block_rows;   /* output rows per y-aggregation tile */
   int32_t cax_pitch;          /* row pitch (elements) of the CA_x volumes */
@@ -158,8 +158,11 @@ int stereo_get_tables(const stereo_t* h, uint32_t* qad, uint32_t* qmc, uint32_t*
  *   STEREO_BUF_PIX_L/R : u16 [Hs][Ws]  = I | census << 8  (scaled image + code)
  *   STEREO_BUF_ARM_L/R : u32 [Hs][Ws]  = m | n << 8 | M << 16 | N << 24
  *                        (m, n: -x/+x arms; M, N: -y/+y arms)
- *   STEREO_BUF_CAX_L/R : u32 [Ds][Hs][Wp]  Eq. 7 (fixed point); Wp = cax_pitch
- *                        = Ws rounded up to 32 (columns >= Ws are undefined)
+ *   STEREO_BUF_CAX_L/R : u32 [ceil(Ds/2)][Hs][Wp][2]  Eq. 7 (fixed point),
+ *                        disparities 2j and 2j+1 interleaved per pixel (the
+ *                        x pass stores, the y pass TMA-loads disparity pairs);
+ *                        Wp = cax_pitch = Ws rounded up to 32 (columns >= Ws
+ *                        and the odd-Ds tail slot are undefined)
  *   STEREO_BUF_CA_L/R  : u64 [Ds][Hs][Ws]  Eq. 8, only after
  *                        stereo_set_debug(h, STEREO_DEBUG_CA, 1)
  *   STEREO_BUF_DL/DR   : u8  [Hs][Ws]  Eq. 9 WTA maps

@@ -232,8 +232,8 @@ class Stereo:
         return {
             BUF_PIX_L: (n2, np.uint16), BUF_PIX_R: (n2, np.uint16),
             BUF_ARM_L: (n2, np.uint32), BUF_ARM_R: (n2, np.uint32),
-            BUF_CAX_L: ((i.Ds, i.Hs, i.cax_pitch), np.uint32),
-            BUF_CAX_R: ((i.Ds, i.Hs, i.cax_pitch), np.uint32),
+            BUF_CAX_L: (((i.Ds + 1) // 2, i.Hs, i.cax_pitch, 2), np.uint32),
+            BUF_CAX_R: (((i.Ds + 1) // 2, i.Hs, i.cax_pitch, 2), np.uint32),
             BUF_CA_L: ((i.Ds, i.Hs, i.Ws), np.uint64), BUF_CA_R: ((i.Ds, i.Hs, i.Ws), np.uint64),
             BUF_DL: (n2, np.uint8), BUF_DR: (n2, np.uint8), BUF_MASKED: (n2, np.uint8),
             BUF_MEDIAN: (n2, np.uint8), BUF_FILL: (n2, np.float32),
@@ -241,13 +241,23 @@ class Stereo:
         }[buf]
 
     def download(self, buf):
+        """Host copy of a stage buffer; CA_x volumes come back as [Ds][Hs][pitch]
+        (the device interleaves disparity pairs, see include/stereo.h)."""
         shp, dt = self._shape(buf)
         a = np.zeros(shp, dt)
         _check(lib().stereo_debug_download(self._h, buf, a.ctypes.data, a.nbytes))
+        if buf in (BUF_CAX_L, BUF_CAX_R):
+            i = self.info
+            a = a.transpose(0, 3, 1, 2).reshape(-1, i.Hs, i.cax_pitch)[:i.Ds].copy()
         return a
 
     def upload(self, buf, arr):
         shp, dt = self._shape(buf)
+        if buf in (BUF_CAX_L, BUF_CAX_R):  # [Ds][Hs][pitch] -> disparity pairs interleaved
+            i = self.info
+            v = np.zeros((shp[0] * 2, i.Hs, i.cax_pitch), dt)
+            v[:i.Ds] = np.asarray(arr, dtype=dt).reshape(i.Ds, i.Hs, i.cax_pitch)
+            arr = v.reshape(shp[0], 2, i.Hs, i.cax_pitch).transpose(0, 2, 3, 1)
         a = np.ascontiguousarray(arr, dtype=dt).reshape(shp)
         _check(lib().stereo_debug_upload(self._h, buf, a.ctypes.data, a.nbytes))
 

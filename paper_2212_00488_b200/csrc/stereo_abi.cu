@@ -206,7 +206,7 @@ struct BufView {
 BufView buf_view(stereo_t* h, int id) {
   const Geom& g = h->g;
   const size_t n = (size_t)g.Ws * g.Hs;
-  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
   switch (id) {
     case STEREO_BUF_PIX_L: return {h->b.pixL, n * 2};
     case STEREO_BUF_PIX_R: return {h->b.pixR, n * 2};
@@ -288,7 +288,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   }
   build_tables(*p, g.f, h->qad_h, h->qmc_h);
   const size_t n = (size_t)g.Ws * g.Hs;
-  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
   Buffers& b = h->b;
   struct A { void** p; size_t bytes; } as[] = {
       {(void**)&b.pixL, n * 2 + 16}, {(void**)&b.pixR, n * 2 + 16}, {(void**)&b.armL, n * 4},
@@ -409,7 +409,7 @@ int stereo_get_info(const stereo_t* h, stereo_info* info) {
   info->device = h->device;
   uint64_t tot = 0;
   const size_t n = (size_t)g.Ws * g.Hs;
-  const size_t vol = (size_t)g.Ds * g.Hs * g.Wp;
+  const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
   tot += n * (2 + 2 + 4 + 4 + 1 + 1 + 1 + 1 + 4) + vol * 8 + (size_t)g.Hs * 8 + 263 * 4;
   if (g.K == 2) tot += 2 * n;
   info->device_bytes = tot;

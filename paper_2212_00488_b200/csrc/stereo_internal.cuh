@@ -34,7 +34,7 @@ struct Buffers {
   uint32_t* armR = nullptr;
   uint32_t* xrow = nullptr;  // u32 [4][Hs][Wp] x-pass rows: code L, code R (census | I << 24),
                              // window byte offsets L, R (4(x-m) | 4(x+n+1) << 16)
-  uint32_t* caxL = nullptr;  // u32 [Ds][Hs][Wp]
+  uint32_t* caxL = nullptr;  // u32 [ceil(Ds/2)][Hs][Wp][2] (disparity pairs interleaved)
   uint32_t* caxR = nullptr;
   uint64_t* caL = nullptr;   // debug only: u64 [Ds][Hs][Ws]
   uint64_t* caR = nullptr;
@@ -71,7 +71,7 @@ struct Plan {
   int ypass_nb = 0;  // tiles per column strip
   int ypass_SEG = 0; // tile rows per warp; TMA box height = 8*SEG
   int ypass_smem = 0;
-  CUtensorMap tmL, tmR;  // 3-D maps over the CA_x volumes {Wp, Hs, Ds}
+  CUtensorMap tmL, tmR;  // 3-D u64 maps over the CA_x volumes {Wp, Hs, ceil(Ds/2)}
   int post_smem = 0;
   int post_rows = 2;     // scaled rows per POST CTA
   int post_threads = 512;

@@ -458,7 +458,7 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
 // (x, d+1) is the one of (x-1, d), so both cost rows come from the same C + 1
 // shared loads per lane, both window sets from the same offsets, and the two
 // shuffle scans overlap.
-// Output layout: u32 [Ds][Hs][Wp] (Wp = 32C).
+// Output layout: u32 [ceil(Ds/2)][Hs][Wp][2] (disparity pairs interleaved; Wp = 32C).
 // ============================================================================
 struct XArgs {
   const uint32_t* xrow;  // [4][Hs][Wp]
@@ -507,12 +507,16 @@ __device__ __forceinline__ void xpass_load_row(uint32_t* slot, uint64_t* bar, co
 
 // Phase C of an item: CA_x of the lane's columns x = lane + 32 i for both
 // bases from the exclusive prefix rows (L: P_d, P_{d+1}; R: the same rows
-// shifted by d, resp. d + 1), one coalesced 128-B store per warp and output row.
-template <int C, bool TWO>
+// shifted by d, resp. d + 1); the pair (d, d+1) of a pixel is one 8-B store
+// (CA_x layout u32 [Ds/2][Hs][Wp][2]), 256 coalesced bytes per warp.
+// MODE 2: disparities d and d+1 (one 8-B store per pixel); 1: d only, the
+// d+1 slot zero (odd-Ds tail of the two-disparity kernel); 0: d only, a 4-B
+// store into slot d & 1 (the one-disparity kernel for very wide images).
+template <int C, int MODE>
 __device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_t* sAR,
                                               const char* P0, const char* P0d, const char* P1,
-                                              const char* P1d, uint32_t* outL, uint32_t* outR,
-                                              size_t dstep, int lane) {
+                                              const char* P1d, uint2* outL, uint2* outR, int lane,
+                                              int slot) {
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
@@ -521,15 +525,18 @@ __device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_
                          *reinterpret_cast<const uint32_t*>(P0 + alo);
     const uint32_t caR = *reinterpret_cast<const uint32_t*>(P0d + arhi) -
                          *reinterpret_cast<const uint32_t*>(P0d + arlo);
-    outL[32 * i] = caL;  // pitch Wp = 32C: padding columns are written, never read
-    outR[32 * i] = caR;
-    if (TWO) {
-      const uint32_t caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) -
-                            *reinterpret_cast<const uint32_t*>(P1 + alo);
-      const uint32_t caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) -
-                            *reinterpret_cast<const uint32_t*>(P1d + arlo);
-      outL[dstep + 32 * i] = caL1;
-      outR[dstep + 32 * i] = caR1;
+    // pitch Wp = 32C: padding columns are written, never read
+    if (MODE == 0) {
+      reinterpret_cast<uint32_t*>(outL + 32 * i)[slot] = caL;
+      reinterpret_cast<uint32_t*>(outR + 32 * i)[slot] = caR;
+    } else {
+      uint32_t caL1 = 0u, caR1 = 0u;
+      if (MODE == 2) {
+        caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) - *reinterpret_cast<const uint32_t*>(P1 + alo);
+        caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) - *reinterpret_cast<const uint32_t*>(P1d + arlo);
+      }
+      outL[32 * i] = make_uint2(caL, caL1);
+      outR[32 * i] = make_uint2(caR, caR1);
     }
   }
 }
@@ -642,14 +649,15 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     }
     __syncwarp();
     // ---- phase C: window differences (precomputed byte offsets), coalesced stores
-    uint32_t* outL = a.caxL + ((size_t)d * a.Hs + y) * a.Wp + lane;
-    uint32_t* outR = a.caxR + ((size_t)d * a.Hs + y) * a.Wp + lane;
-    const size_t dstep = (size_t)a.Hs * a.Wp;
+    uint2* outL = reinterpret_cast<uint2*>(a.caxL) + ((size_t)(d >> 1) * a.Hs + y) * a.Wp + lane;
+    uint2* outR = reinterpret_cast<uint2*>(a.caxR) + ((size_t)(d >> 1) * a.Hs + y) * a.Wp + lane;
     const char* Pdb = Pb + 4 * d;
-    if (ND == 2 && two)  // (the single-disparity tail item exists only for odd Ds)
-      xpass_windows<C, true>(sAL, sAR, Pb, Pdb, Pb + PLb, Pdb + PLb + 4, outL, outR, dstep, lane);
+    if (ND == 1)
+      xpass_windows<C, 0>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, lane, d & 1);
+    else if (two)  // (the single-disparity tail item exists only for odd Ds)
+      xpass_windows<C, 2>(sAL, sAR, Pb, Pdb, Pb + PLb, Pdb + PLb + 4, outL, outR, lane, 0);
     else
-      xpass_windows<C, false>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, dstep, lane);
+      xpass_windows<C, 1>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, lane, 0);
     __syncwarp();
     // ---- release the row slot: the warp finishing the row's last item of
     // this range refills the slot with the row `slots` ahead
@@ -893,7 +901,7 @@ __global__ void __launch_bounds__(kYThreads, 2)
                  YArgs a) {
   static_assert(SEG & 1, "SEG must be odd (bank-disjoint half-warps)");
   constexpr int TB = kYSegs * SEG;                 // tile rows = TMA box height
-  constexpr uint32_t kTileBytes = 2 * TB * 16 * 4;  // box {16, TB, 2}
+  constexpr uint32_t kTileBytes = 2 * TB * 16 * 4;  // box {16 columns, TB rows, 1 pair} of u64
   extern __shared__ __align__(128) uint8_t ysm[];  // TMA destinations need 128-B alignment
   uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                      // [kYStages][2][TB][16]
   uint2* Elo = reinterpret_cast<uint2*>(ysm + kYStages * kTileBytes);      // [TB+1][16]
@@ -926,7 +934,7 @@ __global__ void __launch_bounds__(kYThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kYStages && 2 * s < Ds; ++s) {
       mbar_expect_tx(bar + s, kTileBytes);
-      tma_load_3d(tile + s * 2 * TB * 16, tm, bar + s, x0, yt0, 2 * s);
+      tma_load_3d(tile + s * 2 * TB * 16, tm, bar + s, x0, yt0, s);
     }
   }
   if (tid < 16) {
@@ -960,13 +968,14 @@ __global__ void __launch_bounds__(kYThreads, 2)
   for (int d = 0; d < Ds; d += 2) {
     const int it = d >> 1, st = it & 1;
     mbar_wait(bar + st, (it >> 1) & 1);
-    const uint32_t* t0 = tile + st * 2 * TB * 16 + seg * SEG * 16 + col;
-    const uint32_t* t1 = t0 + TB * 16;
+    // tile rows hold (d, d+1) pairs per column: one 8-B load per element
+    const uint2* t01 = reinterpret_cast<const uint2*>(tile + st * 2 * TB * 16) + seg * SEG * 16 + col;
     uint32_t l0[SEG], l1[SEG], lh[SEG];
     uint32_t a0 = 0, a1 = 0, ah = 0;
 #pragma unroll
     for (int s = 0; s < SEG; ++s) {
-      const uint32_t v0 = t0[s * 16], v1 = t1[s * 16];
+      const uint2 v = t01[s * 16];
+      const uint32_t v0 = v.x, v1 = v.y;
       a0 += v0 & kLoMask;
       a1 += v1 & kLoMask;
       ah += __byte_perm(v0, 0u, 0x4443u) + __byte_perm(v1, 0u, 0x4344u);  // v0.b3 | v1.b3 << 16
@@ -980,7 +989,7 @@ __global__ void __launch_bounds__(kYThreads, 2)
     if (tid == 0 && d + 2 * kYStages < Ds) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar + st, kTileBytes);
-      tma_load_3d(tile + st * 2 * TB * 16, tm, bar + st, x0, yt0, d + 2 * kYStages);
+      tma_load_3d(tile + st * 2 * TB * 16, tm, bar + st, x0, yt0, (d >> 1) + kYStages);
     }
     uint32_t o0 = upper ? b0 : 0u, o1 = upper ? b1 : 0u, oh = upper ? bh : 0u;
     // earlier warps' totals: unrolled, warp-uniform predicates, so that all
@@ -1593,8 +1602,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows,
-                             int box_d) {
+// 3-D map over a CA_x volume as u64 elements (the (d, d+1) pair of a pixel):
+// {Wp columns, Hs rows, ceil(Ds/2) pairs}; box {16 columns, box_rows, 1 pair}
+static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1604,11 +1614,11 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
     if (q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
     fn = reinterpret_cast<EncodeTiledFn>(f);
   }
-  cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)g.Ds};
-  cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 4, (cuuint64_t)g.Wp * g.Hs * 4};
-  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, (cuuint32_t)box_d};
+  cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)((g.Ds + 1) / 2)};
+  cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 8, (cuuint64_t)g.Wp * g.Hs * 8};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -1732,8 +1742,8 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     if (e != cudaSuccess) return e;
     p.xpass_grid = nsm;
   }
-  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG, 2))) return e;
-  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG, 2))) return e;
+  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG))) return e;
+  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG))) return e;
   return cudaSuccess;
 }
 
