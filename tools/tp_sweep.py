@@ -11,8 +11,8 @@ import torch  # noqa: E402
 
 from paper_2212_00488_b200 import abi, synth  # noqa: E402
 
-W, H, D, K = 1436, 992, 145, 2
-POOL = 16
+W, H, D, K = [int(v) for v in os.environ.get("TP_WHDK", "1436,992,145,2").split(",")]
+POOL = 16 if W * H <= 4e6 else 4
 frames = [synth.scene(W, H, D, seed=s)[:2] for s in range(POOL)]
 Ls = [torch.from_numpy(f[0]).cuda() for f in frames]
 Rs = [torch.from_numpy(f[1]).cuda() for f in frames]
