@@ -383,18 +383,114 @@ def run_ours(args):
     return 0
 
 
+def run_c5_bands(args):
+    """--workload c5 (BASELINE config c5): ONE 2872x1984, D=290
+    frame per step split into N row bands, one per rank; every step exchanges
+    the input halo rows with the neighbouring ranks (one grouped NCCL send/recv
+    over NVLink), computes the band with the unchanged pipeline and applies the
+    global fill rule (d) if some band needs it (paper_2212_00488_b200/dist.py).
+    "scaling": "strong" (the frame is fixed).  Not the driver's default leg."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2212_00488_b200 import dist as sdist
+    from paper_2212_00488_b200 import synth
+
+    W5, H5, D5 = 2872, 1984, 290
+    ws, rank, local = _dist()
+    backend = os.environ.get("STEREO_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    cdev = torch.device("cpu") if backend == "gloo" else dev  # communication device
+
+    class _Single:  # the dist API for one rank
+        @staticmethod
+        def get_rank():
+            return 0
+
+        @staticmethod
+        def get_world_size():
+            return 1
+
+        @staticmethod
+        def all_reduce(t, op=None):
+            return t
+
+    dd = dist if ws > 1 else _Single
+    nf = 4
+    frames = [synth.scene(W5, H5, D5, seed=500 + i)[:2] for i in range(nf)]
+    bs = sdist.BandStereo(W5, H5, D5, ws, rank)
+    a0, a1 = sdist.owned_rows(bs.b, H5, bs.K)
+    own = [(torch.from_numpy(np.ascontiguousarray(L[a0:a1])).to(cdev),
+            torch.from_numpy(np.ascontiguousarray(R[a0:a1])).to(cdev)) for L, R in frames]
+
+    def step(i):
+        Lo, Ro = own[i % nf]
+        if ws > 1:
+            sdist.run_band_frame(Lo, Ro, W5, H5, D5, dd, dev, stereo=bs)
+        else:  # one band = the whole frame; no exchange
+            out = torch.empty((H5, W5), dtype=torch.float32, device=dev)
+            bs.compute(Lo, Ro, out)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    steps = max(1, min(args.steps, 200))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=cdev)
+    if ws > 1:
+        dist.barrier()
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_max = float(ms.item())
+    if rank == 0:
+        fps = steps / (ms_max / 1e3)
+        print(json.dumps({
+            "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 fixed-point (f32 fill/scale-up)",
+            "data": "synthetic",
+            "config": {"workload": "c5: 2872x1984, D=290, K=2 -> 1436x992, D_s=145; one frame per step "
+                                   f"in {ws} row band(s) with a per-frame halo exchange",
+                       "parallelism": f"row bands x{ws}", "band_rows_scaled": bs.b.ys1 - bs.b.ys0},
+            "gdisp_evals_per_s": fps * W5 * H5 * D5 / 1e9,
+            "e2e": None, "gpu_launches": None,
+        }))
+    bs.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("c3", "c5"), default="c3",
+                    help="c3: frame batches (default, the driver's leg); c5: one high-res "
+                         "frame per step in row bands across the ranks")
     ap.add_argument("--streams", type=int, default=6,
                     help="frames in flight per GPU (one handle per stream)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    return run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_c5_bands(args) if args.workload == "c5" else run_ours(args)
 
 
 if __name__ == "__main__":

@@ -218,18 +218,23 @@ def run_band_frame(L_own, R_own, W, H, D, dist, device, stereo: BandStereo | Non
                    **overrides):
     """One frame in band mode on this rank: exchange halos, compute the band,
     fix rule (d) globally if any band needs it; returns this rank's own output
-    rows (f32 [o1-o0][W], device) and the BandStereo (reusable)."""
+    rows (f32 [o1-o0][W], device) and the BandStereo (reusable).  The
+    exchange runs on L_own's device (CUDA for NCCL; CPU for gloo, whose bands
+    are then copied to `device`)."""
     import torch
     rank, P = dist.get_rank(), dist.get_world_size()
     bs = stereo or BandStereo(W, H, D, P, rank, **overrides)
+    cdev = L_own.device
     Lb, Rb = exchange_halos(L_own, R_own, bs.bands, rank, H, bs.K, dist)
+    if Lb.device != torch.device(device):
+        Lb, Rb = Lb.to(device), Rb.to(device)
     out = torch.empty((bs.b.rows, W), dtype=torch.float32, device=device)
     bs.compute(Lb, Rb, out)
     torch.cuda.synchronize(device)
-    flag = torch.tensor([1 if bs.needs_patch_local() else 0], device=device)
+    flag = torch.tensor([1 if bs.needs_patch_local() else 0], device=cdev)
     dist.all_reduce(flag, op=dist.ReduceOp.MAX)
     if int(flag.item()):
-        summ = gather_row_summaries(bs.local_summaries(), bs.b, H // bs.K, dist, device)
+        summ = gather_row_summaries(bs.local_summaries(), bs.b, H // bs.K, dist, cdev)
         bs.patch(summ, Lb, out)
     return out[bs.own_slice()], bs
 
