@@ -469,6 +469,7 @@ struct XArgs {
   int Ws, Hs, Ds, Wp, PL, ext;
   uint32_t border;
   int slots;  // row slots in the ring (2..kXMaxSlots)
+  uint32_t mc_mask;  // 63, as a parameter (see the Q_MC address below)
 };
 
 constexpr int kXMaxWarps = 16;
@@ -581,6 +582,10 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   // (cL ^ cR)*128 = ((pl ^ pr) & 63) << 7: table addresses in two ALU operations.
   const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
   const char* qmcb = reinterpret_cast<const char*>(sQMC + lane);
+  // the census mask arrives as a kernel parameter so that it sits in a
+  // register: (pl ^ pr) & mask is then one 3-input LOP3 and the table address
+  // one LEA (a literal 63 lets the compiler shift first and mask 0x1f80 after)
+  const uint32_t mcm = a.mc_mask;
   const char* Pb = reinterpret_cast<const char*>(P);
   const int PLb = 4 * a.PL;
   const int Ws = a.Ws;
@@ -609,12 +614,12 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     for (int k = 0; k < C; ++k) {
       const uint32_t pl = Lr[k], pr = Rr[k];
       const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
-      const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & 63u) << 7));
+      const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & mcm) << 7));
       run[0] += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
       pref[0][k] = run[0];
       if (ND == 2) {
         const uint32_t qa1 = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, prv) >> 17));
-        const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & 63u) << 7));
+        const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & mcm) << 7));
         run[ND - 1] += (k < nb + 1) ? border : qa1 + qm1;
         pref[ND - 1][k] = run[ND - 1];
         prv = pr;
@@ -688,7 +693,7 @@ constexpr int xpass_nd() { return C <= kXMaxC2 ? 2 : 1; }
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots};
+          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots, 63u};
   xpass_kernel<C, xpass_nd<C>()><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
