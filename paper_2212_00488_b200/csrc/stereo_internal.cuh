@@ -65,6 +65,7 @@ struct Plan {
   int xpass_grid = 0;
   int xpass_smem = 0;
   int xpass_PL = 0;  // per-warp prefix buffer length
+  bool xpass_fixpl = false;  // PL = 32C + 128 at compile time (small D_s + w_x)
   int xpass_warps = 0;
   int xpass_slots = 3;  // row slots of the bulk-copy ring
   int ypass_B = 0;   // output rows per tile (<= 8*kYRPT)

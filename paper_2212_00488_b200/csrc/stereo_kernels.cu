@@ -542,9 +542,14 @@ __device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_
   }
 }
 
-template <int C, int ND>
+// FIXPL: the per-disparity prefix rows have the compile-time pitch 32C + 128
+// (usable when D_s + w_x + 3 <= 128), so that P_{d+1} = P_d + constant folds
+// into the shared-load immediates instead of one add per window read.
+constexpr int kXFixExt = 128;
+template <int C, int ND, bool FIXPL>
 __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   static_assert(ND == 1 || ND == 2, "one or two disparities per item");
+  const int PL = FIXPL ? 32 * C + kXFixExt : a.PL;
   extern __shared__ __align__(128) uint32_t xsm[];
   uint32_t* sQAD = xsm;                // [256][32]  Q_AD[|dI|], one copy per bank
   uint32_t* sQMC = sQAD + 256 * 32;    // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
@@ -552,10 +557,10 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   const int nw = blockDim.x >> 5;
   const int nslot = a.slots;
   uint32_t* Pall = ring + nslot * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
-  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * a.PL);  // [slots]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * PL);  // [slots]
   unsigned* done = reinterpret_cast<unsigned*>(full + kXMaxSlots);             // [slots]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* P = Pall + warp * ND * a.PL;
+  uint32_t* P = Pall + warp * ND * PL;
 
   // this CTA's item range [i0, i1) of the Hs * npairs items, and its rows
   const int npairs = (a.Ds + ND - 1) / ND;
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   // one LEA (a literal 63 lets the compiler shift first and mask 0x1f80 after)
   const uint32_t mcm = a.mc_mask;
   const char* Pb = reinterpret_cast<const char*>(P);
-  const int PLb = 4 * a.PL;
+  const int PLb = 4 * PL;
   const int Ws = a.Ws;
   const uint32_t border = a.border;
 
@@ -639,18 +644,18 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
 #pragma unroll
     for (int n = 0; n < ND; ++n) {
       const uint32_t off = incl[n] - run[n];
-      uint32_t* Pl = P + n * a.PL + lane * C + 1;
+      uint32_t* Pl = P + n * PL + lane * C + 1;
 #pragma unroll
       for (int k = 0; k < C; ++k) Pl[k] = pref[n][k] + off;
     }
-    if (lane < ND) P[lane * a.PL] = 0;
+    if (lane < ND) P[lane * PL] = 0;
     __syncwarp();
     uint32_t PW[ND];
 #pragma unroll
-    for (int n = 0; n < ND; ++n) PW[n] = P[n * a.PL + Ws];
+    for (int n = 0; n < ND; ++n) PW[n] = P[n * PL + Ws];
     for (int e = lane; e < a.ext; e += 32) {
 #pragma unroll
-      for (int n = 0; n < ND; ++n) P[n * a.PL + Ws + 1 + e] = PW[n] + (uint32_t)(e + 1) * border;
+      for (int n = 0; n < ND; ++n) P[n * PL + Ws + 1 + e] = PW[n] + (uint32_t)(e + 1) * border;
     }
     __syncwarp();
     // ---- phase C: window differences (precomputed byte offsets), coalesced stores
@@ -694,13 +699,19 @@ template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
           g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots, 63u};
-  xpass_kernel<C, xpass_nd<C>()><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
+  if (p.xpass_fixpl)
+    xpass_kernel<C, xpass_nd<C>(), true><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
+  else
+    xpass_kernel<C, xpass_nd<C>(), false><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int C>
 static cudaError_t setup_xpass_c(int smem) {
-  return cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>()>,
+  cudaError_t e = cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), false>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
@@ -1719,7 +1730,8 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
-  p.xpass_PL = 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
+  p.xpass_fixpl = g.Ds + g.w_x_max + 3 <= kXFixExt;
+  p.xpass_PL = p.xpass_fixpl ? 32 * p.xpass_C + kXFixExt : 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
   {
     const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
     // Co-residency: with frames in flight on several streams, an x pass of one
