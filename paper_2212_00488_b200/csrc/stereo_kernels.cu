@@ -47,6 +47,37 @@ __global__ void __launch_bounds__(256) sd_kernel(const uint8_t* __restrict__ Lor
   const int y = blockIdx.x;
   const int Wq = (W + 3) & ~3;
   const bool vec = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 3) == 0);
+  if (M == 1 && vec) {
+    // 3x3 case on aligned rows: stage the three-row COLUMN sums (u16, two per
+    // word, summed as u16x2 lanes: <= 765, no carries), then every output is
+    // cs(2x-1) + cs(2x) + cs(2x+1) (cs(-1) = cs(0); 2x+1 <= W-1 always)
+    uint16_t* cs = reinterpret_cast<uint16_t*>(sdm32);
+    const uint32_t* r0 = reinterpret_cast<const uint32_t*>(src + (size_t)clampi(2 * y - 1, 0, H - 1) * W);
+    const uint32_t* r1 = reinterpret_cast<const uint32_t*>(src + (size_t)(2 * y) * W);
+    const uint32_t* r2 = reinterpret_cast<const uint32_t*>(src + (size_t)clampi(2 * y + 1, 0, H - 1) * W);
+    for (int i = threadIdx.x; i < (W >> 2); i += blockDim.x) {
+      const uint32_t a = __ldg(r0 + i), b = __ldg(r1 + i), c = __ldg(r2 + i);
+      const uint32_t ev = __byte_perm(a, 0, 0x4240) + __byte_perm(b, 0, 0x4240) + __byte_perm(c, 0, 0x4240);
+      const uint32_t od = __byte_perm(a, 0, 0x4341) + __byte_perm(b, 0, 0x4341) + __byte_perm(c, 0, 0x4341);
+      reinterpret_cast<uint2*>(cs)[i] = make_uint2(__byte_perm(ev, od, 0x5410), __byte_perm(ev, od, 0x7632));
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; 2 * t < Ws; t += blockDim.x) {
+      const uint2 q = reinterpret_cast<const uint2*>(cs)[t];  // cs(4t .. 4t+3)
+      const int c0 = q.x & 0xffff, c1 = q.x >> 16, c2 = q.y & 0xffff, c3 = q.y >> 16;
+      const int cm = t ? cs[4 * t - 1] : c0;
+      const int s0 = cm + c0 + c1, s1 = c1 + c2 + c3;
+      const uint32_t o0 = (uint32_t)((2 * s0 + N) / (2 * N)), o1 = (uint32_t)((2 * s1 + N) / (2 * N));
+      uint8_t* d = dst + (size_t)y * Ws + 2 * t;
+      if (2 * t + 1 < Ws && (Ws & 1) == 0) {
+        *reinterpret_cast<uint16_t*>(d) = (uint16_t)(o0 | o1 << 8);
+      } else {
+        d[0] = (uint8_t)o0;
+        if (2 * t + 1 < Ws) d[1] = (uint8_t)o1;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     const uint8_t* row = src + (size_t)clampi(2 * y + j - M, 0, H - 1) * W;
