@@ -1695,11 +1695,13 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   }
   const int Wsp = post_pitch(g.Ws);
   const int Wx = (g.W + 3) & ~3;
-  // 2 rows x 512 threads per CTA: measured best at c2/c3 among {1,2,4} x {256,512}
-  p.post_rows = env_int("STEREO_POST_ROWS", 2, 1, 8);
+  // 4 rows x 384 threads per CTA: best throughput with frames in flight at c2
+  // and c3 among {1,2,4,8} x {256,384,512} (a lone frame is ~2% slower than
+  // with 2 x 512)
+  p.post_rows = env_int("STEREO_POST_ROWS", 4, 1, 8);
   if (p.post_rows == 3) p.post_rows = 2;
   if (p.post_rows > 4) p.post_rows = 8;
-  p.post_threads = env_int("STEREO_POST_THREADS", 512, 128, 512) & ~127;
+  p.post_threads = env_int("STEREO_POST_THREADS", 384, 128, 512) & ~127;
   // step 4 of POST runs one warp per fill row (R + 1 of them)
   p.post_threads = std::max(p.post_threads, (32 * (p.post_rows + 1) + 127) & ~127);
   {
