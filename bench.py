@@ -278,10 +278,10 @@ def run_ours(args):
     fps = ws * args.steps / (ms_max / 1e3)
 
     # ---- end to end through the public C ABI with HOST buffers (pinned):
-    # H2D of L, R + compute + D2H of the disparity map, every step, on the same
-    # number of streams / handles as the device-resident run (at least two) so
+    # H2D of L, R + compute + D2H of the disparity map, every step, on
+    # --e2e-streams handles / streams (at least the device-resident count) so
     # the copies overlap other frames' kernels.
-    NE = max(NS, 2)
+    NE = max(NS, args.e2e_streams, 2)
     extra = [abi.Stereo(W, H, D) for _ in range(NE - NS)]
     e2e_h = list(handles) + extra
     e2e_s = [torch.cuda.Stream(dev) for _ in range(NE)]
@@ -357,7 +357,7 @@ def run_ours(args):
                              f"({POOL * W * H * 2 / 1e6:.0f} MB) + {2 * vol / 1e6:.0f} MB CA_x "
                              "written and read per frame",
                        "parallelism": f"frame-batch dp{ws}" if ws > 1 else "single GPU",
-                       "streams_per_gpu": NS,
+                       "streams_per_gpu": NS, "e2e_streams_per_gpu": NE,
                        "ms_per_step_single_stream": ms_single},
             "gdisp_evals_per_s": fps * W * H * D / 1e9,
             "executed_gdisp_evals_per_s": fps * 2 * info.Ws * info.Hs * info.Ds / 1e9,
@@ -483,8 +483,12 @@ def main():
     ap.add_argument("--workload", choices=("c3", "c5"), default="c3",
                     help="c3: frame batches (default, the driver's leg); c5: one high-res "
                          "frame per step in row bands across the ranks")
-    ap.add_argument("--streams", type=int, default=6,
-                    help="frames in flight per GPU (one handle per stream)")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="frames in flight per GPU (one handle per stream); measured "
+                         "best of 2..8 at c3: 4")
+    ap.add_argument("--e2e-streams", type=int, default=6,
+                    help="frames in flight for the end-to-end (host buffer) leg: the "
+                         "copies need more overlap (6 measured best)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
