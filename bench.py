@@ -486,9 +486,9 @@ def main():
     ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one handle per stream); measured "
                          "best of 2..8 at c3: 4")
-    ap.add_argument("--e2e-streams", type=int, default=6,
+    ap.add_argument("--e2e-streams", type=int, default=8,
                     help="frames in flight for the end-to-end (host buffer) leg: the "
-                         "copies need more overlap (6 measured best)")
+                         "copies need more overlap (6 / 8 / 12 measured: 7.60 / 7.75 / 7.76 k fps)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
