@@ -627,10 +627,14 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   const int Ws = a.Ws;
   const uint32_t border = a.border;
 
+  // item -> (row y, pair p), row -> (ring slot, lap): one division at the
+  // start, then incremental updates (a warp's items are nw apart, nw < npairs
+  // is not assumed: the row advance is a short loop)
+  int y = (i0 + warp) / npairs, pidx = i0 + warp - y * npairs;
+  int slot = (y - rfirst) % nslot, lap = (y - rfirst) / nslot;
 #pragma unroll 1
   for (int it = i0 + warp; it < i1; it += nw) {
-    const int y = it / npairs, d = (it - y * npairs) * ND;
-    const int rel = y - rfirst, lap = rel / nslot, slot = rel - lap * nslot;
+    const int d = pidx * ND;
     xbar_wait(full + slot, (uint32_t)lap & 1u);
     const uint32_t* sL = ring + slot * 4 * 32 * C;
     const uint32_t* sR = sL + 32 * C;
@@ -711,6 +715,10 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + nslot);
       }
+    }
+    for (pidx += nw; pidx >= npairs; pidx -= npairs) {  // next item of this warp
+      ++y;
+      if (++slot == nslot) { slot = 0; ++lap; }
     }
   }
 }
