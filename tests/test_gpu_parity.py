@@ -171,6 +171,17 @@ def test_prep_arm_caps_extremes(w_x, w_y):
     _compare(L, R, 6, dict(k_scale=1, w_x=w_x, w_y=w_y, delta=20))
 
 
+@pytest.mark.parametrize("W,H,D,kw", [
+    (4032, 40, 60, dict(k_scale=2)),                       # W_s = 2016: widest lane chunk (C = 63)
+    (1000, 30, 510, dict(k_scale=2, w_y=20)),              # D_s = 255: the largest u8 disparity range
+    (300, 260, 40, dict(k_scale=2, w_y=112, w_x=60)),      # w_y = 112: tallest y window
+])
+def test_maximum_sizes_bit_exact(W, H, D, kw):
+    """The ABI's upper limits (W_s <= 2016, D_s <= 255, w_y <= 112) bit-exact."""
+    L, R, _ = synth.scene(W, H, min(D, W // 2), seed=W + D)
+    _compare(L, R, D, kw, volumes=False)
+
+
 def test_c2_quarter_scene_bit_exact():
     L, R, _ = synth.scene(450, 375, 64, seed=1)
     _compare(L, R, 64, dict(k_scale=1))
