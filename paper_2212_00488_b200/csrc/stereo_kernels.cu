@@ -577,6 +577,7 @@ __device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_
 // (usable when D_s + w_x + 3 <= 128), so that P_{d+1} = P_d + constant folds
 // into the shared-load immediates instead of one add per window read.
 constexpr int kXFixExt = 128;
+constexpr int kXMaxC2 = 27;  // widest lane chunk kept in registers in one pass
 template <int C, int ND, bool FIXPL>
 __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   static_assert(ND == 1 || ND == 2, "one or two disparities per item");
@@ -647,24 +648,44 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     // sR (in the slot's sL or the tables: d <= 255) and are unused
     const int nb = d - lane * C;
     const uint32_t* Rr = sR + lane * C - d;
-    uint32_t pref[ND][C];
+    // Register passes of CH columns: one pass when the 2C prefix registers fit
+    // (C <= kXMaxC2), else two (wide rows, C <= 2 kXMaxC2): the first pass's
+    // local prefixes go to shared memory right away and get the lane offset
+    // added after the warp scan (one read-modify-write per element).
+    constexpr int CH = C <= kXMaxC2 ? C : (C + 1) / 2;
+    uint32_t pref[ND][CH];
     uint32_t run[ND] = {};
     uint32_t prv = ND == 2 ? Rr[-1] : 0u;  // right pixel of (x, d+1) = of (x-1, d)
+    auto costs = [&](int k0, int kn) {
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const uint32_t pl = Lr[k], pr = Rr[k];
-      const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
-      const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & mcm) << 7));
-      run[0] += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
-      pref[0][k] = run[0];
-      if (ND == 2) {
-        const uint32_t qa1 = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, prv) >> 17));
-        const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & mcm) << 7));
-        run[ND - 1] += (k < nb + 1) ? border : qa1 + qm1;
-        pref[ND - 1][k] = run[ND - 1];
-        prv = pr;
+      for (int j = 0; j < CH; ++j) {
+        if (j < kn) {
+          const int k = k0 + j;
+          const uint32_t pl = Lr[k], pr = Rr[k];
+          const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
+          const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & mcm) << 7));
+          run[0] += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
+          pref[0][j] = run[0];
+          if (ND == 2) {
+            const uint32_t qa1 = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, prv) >> 17));
+            const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & mcm) << 7));
+            run[ND - 1] += (k < nb + 1) ? border : qa1 + qm1;
+            pref[ND - 1][j] = run[ND - 1];
+            prv = pr;
+          }
+        }
+      }
+    };
+    if (CH < C) {  // first pass, stored without the lane offset
+      costs(0, CH);
+#pragma unroll
+      for (int n = 0; n < ND; ++n) {
+        uint32_t* Pl = P + n * PL + lane * C + 1;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) Pl[j] = pref[n][j];
       }
     }
+    costs(C - CH == 0 ? 0 : CH, C - (CH < C ? CH : 0));
     uint32_t incl[ND];
 #pragma unroll
     for (int n = 0; n < ND; ++n) incl[n] = run[n];
@@ -680,8 +701,15 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     for (int n = 0; n < ND; ++n) {
       const uint32_t off = incl[n] - run[n];
       uint32_t* Pl = P + n * PL + lane * C + 1;
+      if (CH < C) {
 #pragma unroll
-      for (int k = 0; k < C; ++k) Pl[k] = pref[n][k] + off;
+        for (int j = 0; j < CH; ++j) Pl[j] += off;  // first pass: add the offset
+#pragma unroll
+        for (int j = 0; j < C - CH; ++j) Pl[CH + j] = pref[n][j] + off;
+      } else {
+#pragma unroll
+        for (int k = 0; k < C; ++k) Pl[k] = pref[n][k] + off;
+      }
     }
     if (lane < ND) P[lane * PL] = 0;
     __syncwarp();
@@ -729,10 +757,10 @@ int xpass_chunk_for(int Ws) {
   return 0;
 }
 
-// two disparities per item while the 2C prefix registers fit
-constexpr int kXMaxC2 = 27;
+// two disparities per item while the prefix registers of one or two register
+// passes (2 * ceil(C/2)) fit
 template <int C>
-constexpr int xpass_nd() { return C <= kXMaxC2 ? 2 : 1; }
+constexpr int xpass_nd() { return C <= 2 * kXMaxC2 ? 2 : 1; }
 
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
@@ -1774,14 +1802,14 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   p.xpass_fixpl = g.Ds + g.w_x_max + 3 <= kXFixExt;
   p.xpass_PL = p.xpass_fixpl ? 32 * p.xpass_C + kXFixExt : 32 * p.xpass_C + g.Ds + g.w_x_max + 3;
   {
-    const int nd = p.xpass_C <= kXMaxC2 ? 2 : 1;
+    const int nd = p.xpass_C <= 2 * kXMaxC2 ? 2 : 1;
     // Co-residency: with frames in flight on several streams, an x pass of one
     // frame and a y pass of another share each SM when one x-pass CTA of 8
     // warps with a 2-slot ring fits beside one y-pass CTA (registers: 8 + 8
     // warps of <= 128; shared memory: both footprints + the per-CTA reserve).
     // Measured at c3: 143.5 vs 148 us per frame with 6 frames in flight
     // (16 warps / 3 slots alone); a lone frame is ~5% slower.
-    const int nd0 = p.xpass_C <= kXMaxC2 ? 2 : 1;
+    const int nd0 = p.xpass_C <= 2 * kXMaxC2 ? 2 : 1;
     const size_t co = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)2 * 4 * 32 * p.xpass_C +
                                           (size_t)8 * nd0 * p.xpass_PL) +
                       kXMaxSlots * (8 + 4);
