@@ -1814,12 +1814,21 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
                                           (size_t)8 * nd0 * p.xpass_PL) +
                       kXMaxSlots * (8 + 4);
     const bool coresident = co + (size_t)p.ypass_smem + 2 * 1024 <= (size_t)prop.sharedMemPerMultiprocessor;
-    p.xpass_slots = env_int("STEREO_XPASS_SLOTS", coresident ? 2 : 3, 2, kXMaxSlots);
-    const size_t fixed = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 +
-                                             (size_t)p.xpass_slots * 4 * 32 * p.xpass_C) +
-                         kXMaxSlots * (8 + 4);
     const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
     const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
+    auto fixed_for = [&](int slots) {
+      return sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)slots * 4 * 32 * p.xpass_C) +
+             kXMaxSlots * (8 + 4);
+    };
+    // alone: 3 slots, unless shared memory then holds fewer warps than with 2
+    // (wide rows; c5: 2 slots measured 5% faster)
+    int slots_alone = 3;
+    if (fixed_for(3) + per_warp <= cap && fixed_for(2) + per_warp <= cap &&
+        std::min<size_t>(kXMaxWarps, (cap - fixed_for(2)) / per_warp) >
+            std::min<size_t>(kXMaxWarps, (cap - fixed_for(3)) / per_warp))
+      slots_alone = 2;
+    p.xpass_slots = env_int("STEREO_XPASS_SLOTS", coresident ? 2 : slots_alone, 2, kXMaxSlots);
+    const size_t fixed = fixed_for(p.xpass_slots);
     if (fixed + per_warp > cap) return cudaErrorInvalidConfiguration;
     p.xpass_warps = (int)std::min<size_t>(kXMaxWarps, (cap - fixed) / per_warp);
     p.xpass_warps = std::min(p.xpass_warps, env_int("STEREO_XPASS_WARPS", coresident ? 8 : kXMaxWarps, 1, kXMaxWarps));
