@@ -1187,12 +1187,6 @@ struct PostArgs {
   int Wx;   // W rounded up to 4
 };
 
-__device__ __forceinline__ void cswap(int& a, int& b) {
-  const int lo = min(a, b), hi = max(a, b);
-  a = lo;
-  b = hi;
-}
-
 // u16x2 helpers of the SIMD median (lanes hold values 0..255, INVALID = 255)
 __device__ __forceinline__ void cswap16(uint32_t& a, uint32_t& b) {
   const uint32_t lo = __vminu2(a, b), hi = __vmaxu2(a, b);
