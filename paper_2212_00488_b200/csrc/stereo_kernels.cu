@@ -773,13 +773,19 @@ static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cuda
   return cudaGetLastError();
 }
 
+template <typename F>
+static cudaError_t max_carveout(F fn);
+
 template <int C>
 static cudaError_t setup_xpass_c(int smem) {
   cudaError_t e = cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), false>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = max_carveout(xpass_kernel<C, xpass_nd<C>(), true>);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = max_carveout(xpass_kernel<C, xpass_nd<C>(), false>);
+  return e;
 }
 
 #define XPASS_DISPATCH(C_, EXPR)                        \
@@ -1709,6 +1715,19 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
   return std::max(lo, std::min(hi, std::atoi(v)));
 }
 
+// Kernels of different frames share SMs (frames in flight on several
+// streams); an SM whose L1/shared carveout was sized for a small-shared-memory
+// kernel cannot take an x-pass or y-pass CTA until it is reconfigured, so
+// every kernel asks for the maximum shared carveout (STEREO_CARVEOUT = percent,
+// -1 = the driver's default; measured identical on B200 today, where the
+// driver already picks the maximum for these kernels: kept as a guarantee).
+template <typename F>
+static cudaError_t max_carveout(F fn) {
+  const int pct = env_int("STEREO_CARVEOUT", 100, -1, 100);
+  if (pct < 0) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
@@ -1739,12 +1758,17 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     p.post_smem = (R + 3) * Wsp + (R + 1) * Wsp + (R + 1) * Wsp * 4 + (R + 1) * Wx * 4 +
                   3 * (R + 1) * 64 * 4 + (R + 1) * Wsp * 2 + 2 * (R + 3) * Wsp + (R + 1) * Wx + 64;
   }
-  if (p.prep_smem > 48 * 1024) {
-    for (auto fn : {prep_kernel<32, true>, prep_kernel<32, false>, prep_kernel<16, true>,
-                    prep_kernel<16, false>, prep_kernel<8, true>, prep_kernel<8, false>})
-      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.prep_smem)))
-        return e;
+  for (auto fn : {prep_kernel<32, true>, prep_kernel<32, false>, prep_kernel<16, true>,
+                  prep_kernel<16, false>, prep_kernel<8, true>, prep_kernel<8, false>}) {
+    if (p.prep_smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.prep_smem)))
+      return e;
+    if ((e = max_carveout(fn))) return e;
   }
+  for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>, post_kernel<8>})
+    if ((e = max_carveout(fn))) return e;
+  for (auto fn : {sd_kernel<0>, sd_kernel<1>, sd_kernel<2>, sd_kernel<3>})
+    if ((e = max_carveout(fn))) return e;
   if (p.post_smem > 48 * 1024) {
     for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>, post_kernel<8>})
       if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
@@ -1782,6 +1806,10 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     }
   }
   if (!p.ypass_nb) return cudaErrorInvalidValue;
+  YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, false>));
+  if (e != cudaSuccess) return e;
+  YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, true>));
+  if (e != cudaSuccess) return e;
   YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS, false>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        p.ypass_smem));
