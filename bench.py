@@ -367,6 +367,14 @@ def run_ours(args):
                          "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": alg, "pipes": pipes.get(dom.lower())},
             "aggregation_kernels": aggregation,
+            # the measured bound of the dominant kernel: its
+            # shared-memory port, 1 wavefront (128 B) per SM per cycle
+            "roofline_smem": ({"kernel": dom.lower(), "bound": "shared-memory port",
+                               "achieved": pipes[dom.lower()]["smem_wavefronts_per_sm_cycle"],
+                               "peak": 1.0, "unit": "wavefronts/SM/cycle",
+                               "frac": pipes[dom.lower()]["smem_wavefronts_per_sm_cycle"],
+                               "source": "ncu --set full (profiles/ncu_traffic.json)"}
+                              if pipes.get(dom.lower(), {}).get("smem_wavefronts_per_sm_cycle") else None),
             "cpu_baseline": _cpu_baseline() if ws == 1 else None,
             "e2e": {"value": e2e_fps, "unit": "fps", "h2d_bytes_per_step": 2 * W * H,
                     "d2h_bytes_per_step": 4 * W * H, "steps": e2e_steps,
