@@ -69,6 +69,10 @@ int alloc(stereo_t* h, void** p, size_t bytes) {
   if (e != cudaSuccess)
     return fail(STEREO_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
   h->allocs.push_back(*p);
+  // defined contents from the start: the tail paddings that the word loads of
+  // PREP / POST over-read are then initialised (compute-sanitizer initcheck)
+  e = cudaMemset(*p, 0, bytes);
+  if (e != cudaSuccess) return fail(STEREO_ECUDA, "cudaMemset: %s", cudaGetErrorString(e));
   return STEREO_OK;
 }
 

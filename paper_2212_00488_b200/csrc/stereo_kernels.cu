@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   const int nslot = a.slots;
   uint32_t* Pall = ring + nslot * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
   uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * PL);  // [slots]
-  unsigned* done = reinterpret_cast<unsigned*>(full + kXMaxSlots);             // [slots]
+  uint64_t* empty = full + kXMaxSlots;                                          // [slots]
+  unsigned* done = reinterpret_cast<unsigned*>(empty + kXMaxSlots);            // [slots]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* P = Pall + warp * ND * PL;
 
@@ -606,8 +607,16 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   if (threadIdx.x == 0) {
     for (int k = 0; k < nslot; ++k) {
       xbar_init(full + k);
+      // one arrival per item of the slot's row: orders every warp's reads of
+      // the slot before its refill (the counter below only elects the refiller)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + k)), "r"(npairs)
+                   : "memory");
       done[k] = 0u;
     }
+    if (skip0)  // items of the first row owned by earlier CTAs
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(empty)),
+                   "r"(skip0)
+                   : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int k = 0; k < nslot && rfirst + k <= rlast; ++k)
       xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
@@ -735,11 +744,13 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     // ---- release the row slot: the warp finishing the row's last item of
     // this range refills the slot with the row `slots` ahead
     if (lane == 0) {
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot))
+                   : "memory");
       __threadfence_block();
       const unsigned target = (unsigned)((lap + 1) * npairs - (slot == 0 ? skip0 : 0));
       const unsigned prev = atomicAdd(done + slot, 1u);
       if (prev + 1u == target && y + nslot <= rlast) {
-        __threadfence_block();
+        xbar_wait(empty + slot, (uint32_t)lap & 1u);  // complete: this was the last item
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + nslot);
       }
@@ -1834,13 +1845,13 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     const int nd0 = p.xpass_C <= 2 * kXMaxC2 ? 2 : 1;
     const size_t co = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)2 * 4 * 32 * p.xpass_C +
                                           (size_t)8 * nd0 * p.xpass_PL) +
-                      kXMaxSlots * (8 + 4);
+                      kXMaxSlots * (8 + 8 + 4);
     const bool coresident = co + (size_t)p.ypass_smem + 2 * 1024 <= (size_t)prop.sharedMemPerMultiprocessor;
     const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
     const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
     auto fixed_for = [&](int slots) {
       return sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)slots * 4 * 32 * p.xpass_C) +
-             kXMaxSlots * (8 + 4);
+             kXMaxSlots * (8 + 8 + 4);
     };
     // alone: 3 slots, unless shared memory then holds fewer warps than with 2
     // (wide rows; c5: 2 slots measured 5% faster)
