@@ -844,17 +844,18 @@ cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t 
 // ============================================================================
 // YPASS — y aggregation (Eq. 8) + WTA (Eq. 9) for one
 // base, Step5.  CTA = 16-column strip x B output rows, looping over
-// d.  Per d a TMA 3-D box {16 columns, TB = 16*SEG rows, 1 disparity} of the
-// CA_x volume starting at row y0 - w_y lands in shared memory (rows outside
-// the image are zero-filled by the TMA unit: they never enter a window);
-// two stages, mbarrier-completed, refilled as soon as a stage is consumed.
-// Thread (col = t & 15, seg = t >> 4) scans SEG rows of its column serially in
-// registers (u64, exact); the two segments of a warp combine by shuffle, the
-// eight warp totals through shared memory; the exact column prefix E lands in
-// shared memory and every output pixel takes CA = E[y+N+1] - E[y-M] (O(1)
-// instead of O(W_y)) and keeps the running minimum with the paper's strict
-// "<": ties keep the smallest d.  SEG is odd so the two half-warps'
-// tile rows fall in disjoint banks; 16-column strips allow tall tiles (small
+// disparity pairs.  Per pair a TMA 3-D box {16 columns, TB = 16*SEG rows,
+// 1 pair} of u64 (d, d+1) elements of the CA_x volume starting at row y0 - w_y
+// lands in shared memory (rows outside the image are zero-filled by the TMA
+// unit: they never enter a window); two stages, mbarrier-completed, refilled
+// as soon as a stage is consumed.  Thread (col = t & 15, seg = t >> 4) scans
+// SEG rows of its column serially in registers (split precision, exact, see
+// below); the two segments of a warp combine by shuffle, the eight warp
+// totals through shared memory; the exact column prefix E lands in shared
+// memory and every output pixel takes CA = E[y+N+1] - E[y-M] (O(1) instead of
+// O(W_y)) and keeps the running minimum with the paper's strict "<":
+// ties keep the smallest d.  SEG is odd so the two half-warps' hi-prefix
+// stores fall in disjoint banks; 16-column strips allow tall tiles (small
 // halo ratio TB/B) at good grid balance.
 // ============================================================================
 struct YArgs {
