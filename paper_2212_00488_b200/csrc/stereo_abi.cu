@@ -304,6 +304,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       {(void**)&b.patchVals, (size_t)g.Hs * 4},
       {(void**)&b.counter, 16},
       {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
+      {(void**)&b.qtab, (size_t)(256 + 64) * 32 * 4},
   };
   for (auto& a : as) {
     if ((rc = alloc(h, a.p, a.bytes))) { stereo_destroy(h); return rc; }
@@ -319,6 +320,12 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   e = cudaMemset(b.counter, 0, 16);
   if (e == cudaSuccess) e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(b.qmc, h->qmc_h, sizeof h->qmc_h, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {  // the x pass's shared-memory table image (one copy per bank)
+    std::vector<uint32_t> tab((256 + 64) * 32);
+    for (int i = 0; i < 256 * 32; ++i) tab[i] = h->qad_h[i >> 5];
+    for (int i = 0; i < 64 * 32; ++i) tab[256 * 32 + i] = h->qmc_h[__builtin_popcount(i >> 5)];
+    e = cudaMemcpy(b.qtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = plan_kernels(g, h->plan, b, h->device);
   if (e != cudaSuccess) {
     stereo_destroy(h);

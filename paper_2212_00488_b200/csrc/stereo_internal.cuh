@@ -50,6 +50,7 @@ struct Buffers {
   float* fill = nullptr;        // f32 [Hs][Ws]
   uint32_t* qad = nullptr;      // u32 [256]
   uint32_t* qmc = nullptr;      // u32 [7]
+  uint32_t* qtab = nullptr;     // u32 [(256 + 64) * 32]: Q_AD[a] and Q_MC[popc(i)] replicated per bank
   // staging for stereo_compute_host
   uint8_t* inL = nullptr;
   uint8_t* inR = nullptr;

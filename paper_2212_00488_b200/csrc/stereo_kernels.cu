@@ -501,6 +501,7 @@ struct XArgs {
   uint32_t border;
   int slots;  // row slots in the ring (2..kXMaxSlots)
   uint32_t mc_mask;  // 63, as a parameter (see the Q_MC address below)
+  const uint32_t* qtab;  // the replicated tables as laid out in shared memory (40 KB)
 };
 
 constexpr int kXMaxWarps = 16;
@@ -591,7 +592,8 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   uint32_t* Pall = ring + nslot * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
   uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * PL);  // [slots]
   uint64_t* empty = full + kXMaxSlots;                                          // [slots]
-  unsigned* done = reinterpret_cast<unsigned*>(empty + kXMaxSlots);            // [slots]
+  uint64_t* tabbar = empty + kXMaxSlots;                                        // [1]
+  unsigned* done = reinterpret_cast<unsigned*>(tabbar + 1);                     // [slots]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* P = Pall + warp * ND * PL;
 
@@ -617,13 +619,19 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(empty)),
                    "r"(skip0)
                    : "memory");
+    xbar_init(tabbar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the bank-replicated tables arrive pre-built (one 40 KB bulk copy)
+    constexpr uint32_t kTabBytes = (256 + 64) * 32 * 4;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tabbar)),
+                 "r"(kTabBytes)
+                 : "memory");
+    bulk_g2s(sQAD, a.qtab, kTabBytes, tabbar);
     for (int k = 0; k < nslot && rfirst + k <= rlast; ++k)
       xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
   }
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sQAD[i] = __ldg(a.qad + (i >> 5));
-  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) sQMC[i] = __ldg(a.qmc + __popc(i >> 5));
-  __syncthreads();
+  __syncthreads();  // barrier inits visible
+  xbar_wait(tabbar, 0u);
   // with pixels encoded as census | I << 24, |dI|*128 = vabsdiffu4(pl, pr) >> 17 and
   // (cL ^ cR)*128 = ((pl ^ pr) & 63) << 7: table addresses in two ALU operations.
   const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
@@ -776,7 +784,7 @@ constexpr int xpass_nd() { return C <= 2 * kXMaxC2 ? 2 : 1; }
 template <int C>
 static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
   XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots, 63u};
+          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots, 63u, b.qtab};
   if (p.xpass_fixpl)
     xpass_kernel<C, xpass_nd<C>(), true><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   else
@@ -1846,13 +1854,13 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     const int nd0 = p.xpass_C <= 2 * kXMaxC2 ? 2 : 1;
     const size_t co = sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)2 * 4 * 32 * p.xpass_C +
                                           (size_t)8 * nd0 * p.xpass_PL) +
-                      kXMaxSlots * (8 + 8 + 4);
+                      kXMaxSlots * (8 + 8 + 4) + 8;
     const bool coresident = co + (size_t)p.ypass_smem + 2 * 1024 <= (size_t)prop.sharedMemPerMultiprocessor;
     const size_t per_warp = sizeof(uint32_t) * (size_t)nd * p.xpass_PL;
     const size_t cap = (size_t)prop.sharedMemPerBlockOptin;
     auto fixed_for = [&](int slots) {
       return sizeof(uint32_t) * ((size_t)256 * 32 + 64 * 32 + (size_t)slots * 4 * 32 * p.xpass_C) +
-             kXMaxSlots * (8 + 8 + 4);
+             kXMaxSlots * (8 + 8 + 4) + 8;
     };
     // alone: 3 slots, unless shared memory then holds fewer warps than with 2
     // (wide rows; c5: 2 slots measured 5% faster)
