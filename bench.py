@@ -342,8 +342,13 @@ def run_ours(args):
         for k in ("xpass", "ypass"):
             us = stage_ms[k.upper()] / max(nfr, 1) * 1e3
             gbs = algb[k] / (us / 1e6) / 1e9
+            ncu = pipes.get(k) or {}
+            ncu_frac = None
+            if prof.get(k) and ncu.get("duration_ns"):  # DRAM bytes / ncu time / peak
+                ncu_frac = prof[k] / (ncu["duration_ns"] * 1e-9) / 1e9 / peak
             aggregation[k] = {"us": us, "algorithmic_bytes": algb[k], "hbm_gbs": gbs,
-                              "hbm_frac": gbs / peak, "ncu_pipes": pipes.get(k)}
+                              "hbm_frac": gbs / peak, "ncu_dram_hbm_frac": ncu_frac,
+                              "ncu_pipes": pipes.get(k)}
         step_ms = ms_max / args.steps
         line = {
             "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws, "steps": args.steps,
