@@ -33,7 +33,7 @@ for r in rows[2:]:
         "smem_wavefronts_per_sm_cycle": (wf / nsm / cyc) if (wf and cyc) else None,
         "bank_conflict_wavefronts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
         "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
-        "duration_ns": (g("gpu__time_duration.sum") or 0) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(
+        "duration_ns": (g("gpu__time_duration.sum") or 0) * {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(
             units[hdr.index("gpu__time_duration.sum")], 1),
     }
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
