@@ -32,6 +32,16 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 W, H, D, K = 1436, 992, 145, 2
+# frame-batch workloads (BASELINE configs; c4 = the c3 stream, c5 = its own band leg)
+WORKLOADS = {
+    "c1": (64, 48, 16, 1, "c1: 64x48, D=16, K=1 (tiny synthetic scenes)"),
+    "c2": (450, 375, 64, 1, "c2: 450x375, D=64, K=1 (Middlebury-quarter-shaped synthetic scenes)"),
+    "c3": (1436, 992, 145, 2, "c3: 1436x992, D=145, K=2 -> 718x496, D_s=73 "
+                              "(Adirondack(H)-shaped synthetic scenes)"),
+    "c4": (1436, 992, 145, 2, "c4: stream of translating c3 frames (1436x992, D=145, K=2), "
+                              "frame-batched across the GPUs"),
+}
+WORKLOAD_NAME = WORKLOADS["c3"][4]
 METRIC = "fps and Gdisp-evals/s at 1436×992 D=145, 1/2/4/8 B200; % HBM peak"
 PAPER_FPS = 40.0  # GTX 780 Ti, Adirondack(H) 1436x992, Dmax=145
 POOL = 64
@@ -126,11 +136,11 @@ def _frames(n, seed):
 
 
 def _cpu_baseline(budget_s=12.0):
-    """The oracle as it stands, all host cores, on c3 frames for ~budget_s."""
+    """The oracle as it stands, all host cores, on frames of the workload for ~budget_s."""
     import oracle
     from paper_2212_00488_b200 import synth
     L, R, _ = synth.scene(W, H, D, seed=0)
-    p = oracle.params()
+    p = oracle.params(k_scale=K)
     cores = _cores()
     n, t0 = 0, time.perf_counter()
     while True:
@@ -141,7 +151,7 @@ def _cpu_baseline(budget_s=12.0):
             break
     fps = n / el
     return {"value": fps, "unit": "fps", "cores": cores, "kind": "oracle",
-            "sample": f"{n} full c3 frame(s) (1436x992, D=145, K=2) through the CPU oracle, "
+            "sample": f"{n} full frame(s) ({W}x{H}, D={D}, K={K}) through the CPU oracle, "
                       f"fixed-point mode, OpenMP threads={cores}, {el:.1f} s",
             "gdisp_evals_per_s": fps * W * H * D / 1e9}
 
@@ -160,7 +170,7 @@ def run_reference(args):
     import oracle
     from paper_2212_00488_b200 import synth
     L, R, _ = synth.scene(W, H, D, seed=0)
-    p = oracle.params()
+    p = oracle.params(k_scale=K)
     cores = _cores()
     # bounded sample: a band of `rows` original rows per step, sized so that
     # (steps + warmup) steps take about 150 s in total
@@ -181,13 +191,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": fps / PAPER_FPS,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": fps / PAPER_FPS if (W, H, D) == (1436, 992, 145) else None,
         "dtype": "u32/u64 fixed-point (f32 fill/scale-up)", "data": "synthetic",
-        "config": {"workload": "c3: 1436x992, D=145, K=2 (Adirondack(H)-shaped synthetic scene)",
-                   "sample_rows_per_step": rows},
+        "config": {"workload": WORKLOAD_NAME, "sample_rows_per_step": rows},
         "gdisp_evals_per_s": fps * W * H * D / 1e9,
         "cpu_baseline": {"value": fps, "unit": "fps", "cores": cores, "kind": "oracle",
-                         "sample": f"each step: a {rows}-row band (of 992) of a c3 frame through "
+                         "sample": f"each step: a {rows}-row band (of {H}) of a frame through "
                                    f"the CPU oracle (fixed mode, {cores} OpenMP threads); fps = "
                                    f"frame fraction / time"},
         "e2e": {"value": fps, "unit": "fps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -218,7 +227,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
     rdev = torch.device("cpu") if backend == "gloo" else dev  # device of the reduced scalars
     NS = max(1, args.streams)
-    handles = [abi.Stereo(W, H, D) for _ in range(NS)]  # one handle per stream (not re-entrant)
+    handles = [abi.Stereo(W, H, D, k_scale=K) for _ in range(NS)]  # one handle per stream (not re-entrant)
     st = handles[0]
     info = st.info
     frames = _frames(POOL, seed=1000 + rank)
@@ -282,7 +291,7 @@ def run_ours(args):
     # --e2e-streams handles / streams (at least the device-resident count) so
     # the copies overlap other frames' kernels.
     NE = max(NS, args.e2e_streams, 2)
-    extra = [abi.Stereo(W, H, D) for _ in range(NE - NS)]
+    extra = [abi.Stereo(W, H, D, k_scale=K) for _ in range(NE - NS)]
     e2e_h = list(handles) + extra
     e2e_s = [torch.cuda.Stream(dev) for _ in range(NE)]
     nh = 8
@@ -353,10 +362,9 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": fps / PAPER_FPS,
+            "scaling": "weak", "vs_baseline": fps / PAPER_FPS if (W, H, D) == (1436, 992, 145) else None,
             "dtype": "u32/u64 fixed-point (f32 fill/scale-up)", "data": "synthetic",
-            "config": {"workload": "c3: 1436x992, D=145, K=2 -> 718x496, D_s=73 "
-                                   "(Adirondack(H)-shaped synthetic scenes), 1 frame per GPU per step",
+            "config": {"workload": WORKLOAD_NAME + ", 1 frame per GPU per step",
                        "frames_pool": POOL,
                        "l2": f"inputs larger than L2: {POOL}-frame pool "
                              f"({POOL * W * H * 2 / 1e6:.0f} MB) + {2 * vol / 1e6:.0f} MB CA_x "
@@ -493,9 +501,9 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("c3", "c5"), default="c3",
-                    help="c3: frame batches (default, the driver's leg); c5: one high-res "
-                         "frame per step in row bands across the ranks")
+    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c3",
+                    help="c3 (default, the driver's leg) and c1 / c2 / c4: frame batches; "
+                         "c5: one high-res frame per step in row bands across the ranks")
     ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one handle per stream); measured "
                          "best of 2..8 at c3: 4")
@@ -505,6 +513,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    global W, H, D, K, WORKLOAD_NAME
+    if args.workload in WORKLOADS:
+        W, H, D, K, WORKLOAD_NAME = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args)
     return run_c5_bands(args) if args.workload == "c5" else run_ours(args)
