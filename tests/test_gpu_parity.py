@@ -131,6 +131,33 @@ def test_random_small_instances(seed):
     _compare(L, R, D, kw)
 
 
+@pytest.mark.parametrize("seed", range(16))
+def test_random_medium_instances(seed):
+    """Random parameters at sizes with interior tiles (the word-load strip
+    paths of PREP, several x-pass lane chunks, several y-pass bands, several
+    POST CTAs); every stage bit-exact."""
+    rng = np.random.default_rng(5000 + seed)
+    K = int(rng.choice([1, 2]))
+    W = int(rng.integers(160, 420))
+    H = int(rng.integers(90, 220))
+    D = int(rng.integers(8, 72))
+    cand = [(dx, dy) for dx in range(-2, 3) for dy in range(-2, 3) if (dx, dy) != (0, 0)]
+    pat = [cand[i] for i in rng.choice(len(cand), 6, replace=False)] if rng.random() < 0.5 \
+        else list(oracle.DEFAULT_CENSUS)
+    kw = dict(k_scale=K, delta=int(rng.choice([int(rng.integers(1, 60)), int(rng.integers(128, 300))])),
+              w_x=int(rng.integers(0, 45)), w_y=int(rng.integers(0, 45)), t_fill=int(rng.integers(0, 6)),
+              m_pool=int(rng.integers(0, 3)), census=pat)
+    if rng.random() < 0.3:
+        kw["w_x_r"] = int(rng.integers(0, 45))
+    if rng.random() < 0.4:
+        kw["fill_mode"] = int(rng.integers(0, 4))
+    if rng.random() < 0.5:
+        L, R, _ = synth.scene(W, H, max(D * K, 2), seed)
+    else:
+        L, R = synth.random_pair(W, H, seed, levels=int(rng.choice([8, 256])))
+    _compare(L, R, D * K, kw, volumes=False)
+
+
 @pytest.mark.parametrize("W,H,D,K", [
     (33, 17, 40, 1),      # D_s > W_s: every candidate beyond the image for many x
     (737, 9, 64, 1),      # Ws > 736: next lane-chunk template, ragged tail
