@@ -754,7 +754,6 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     if (lane == 0) {
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot))
                    : "memory");
-      __threadfence_block();
       const unsigned target = (unsigned)((lap + 1) * npairs - (slot == 0 ? skip0 : 0));
       const unsigned prev = atomicAdd(done + slot, 1u);
       if (prev + 1u == target && y + nslot <= rlast) {
@@ -1038,14 +1037,14 @@ __global__ void __launch_bounds__(kYThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
+    // the initialising thread may use the barriers at once: first tiles in
+    // flight before the CTA barrier
     for (int s = 0; s < kYStages && 2 * s < Ds; ++s) {
       mbar_expect_tx(bar + s, kTileBytes);
       tma_load_3d(tile + s * 2 * TB * 16, tm, bar + s, x0, yt0, s);
     }
   }
+  __syncthreads();
   if (tid < 16) {
     Elo[tid] = make_uint2(0u, 0u);
     Ehi[tid] = 0u;
