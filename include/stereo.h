@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define STEREO_ABI_VERSION 2u
+#define STEREO_ABI_VERSION 3u
 
 enum {
   STEREO_OK = 0,
@@ -94,6 +94,13 @@ typedef struct {
   int32_t launches_per_frame; /* kernels enqueued by one stereo_compute */
   int32_t ypass_block_rows;   /* output rows per y-aggregation tile */
   int32_t cax_pitch;          /* row pitch (elements) of the CA_x volumes */
+  /* ABI 3 */
+  int32_t max_frames;         /* frames one launch sequence serves (stereo_create_batch) */
+  int32_t band;               /* 1: a row-band handle (stereo_create_band) */
+  int32_t band_y0_org, band_rows_org;          /* band: own original rows */
+  int32_t band_halo_top_org, band_halo_bot_org; /* band: halo rows above / below */
+  int32_t ypass_rows;         /* scaled rows the y aggregation + WTA computes per frame
+                                 (band: own rows + the cross-check / median / Step8 cone) */
 } stereo_info;
 
 typedef struct stereo_s stereo_t; /* opaque; owns ALL device scratch */
@@ -108,12 +115,16 @@ void stereo_default_params(stereo_params* p);
  * W/K >= 1, H/K >= 1, six distinct non-zero census offsets -> STEREO_EINVAL.
  * STEREO_EUNSUPPORTED for K not in {1,2}, ceil(D/K) > 255 (u8 maps use 255 as
  * INVALID), w_x or w_x_r > 254 (u8 arms), w_y > 112 (the y-aggregation tile
- * holds B + 2*w_y <= 240 rows), census offsets beyond +-2, m_pool > 3.
+ * holds B + 2*w_y <= 240 rows), census offsets beyond +-2, m_pool > 3, and
+ * scaled widths W/K > 2016 (the x pass keeps a row in 32 lane chunks of at
+ * most 63 columns).
  * STEREO_EINVAL also for w_x_r < -1 and fill_mode outside STEREO_FILL_*.
  * Allocates every device buffer (dominant: two u32 CA_x volumes of
  * Ds*Hs*Ws*4 bytes each), builds the fixed-point cost tables on the host in
  * double precision and uploads them.  No kernel runs.  On success *out owns
- * the handle (release with stereo_destroy). */
+ * the handle (release with stereo_destroy).  The handle is bound to the CUDA
+ * device current at create: every later call switches to that device for its
+ * own work and restores the caller's current device before returning. */
 int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out);
 
 /* Enqueue one frame on `stream` and return without synchronising.
@@ -126,8 +137,21 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out);
 int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                    void* stream);
 
-/* `nframes` frames back to back; L, R: DEVICE u8 [nframes][H][W]; disp_out:
- * DEVICE f32 [nframes][H][W].  Same contract as stereo_compute. */
+/* As stereo_create, with buffers for up to max_frames frames (>= 1) so that
+ * stereo_compute_batch enqueues each kernel ONCE per chunk of max_frames
+ * frames (SD / census+arms / C+CA_x / CA+WTA / CC+median+fill+SU: five
+ * launches per chunk, K = 2; four for K = 1) instead of once per frame.
+ * Device memory grows linearly with max_frames (stereo_info.device_bytes).
+ * STEREO_EINVAL for max_frames < 1; STEREO_EUNSUPPORTED if
+ * max_frames * H/K > 2^20.  Stage access (debug up/download, run_stage,
+ * set_debug) needs max_frames == 1. */
+int stereo_create_batch(int W, int H, int D, const stereo_params* p, int max_frames,
+                        stereo_t** out);
+
+/* `nframes` (>= 0) frames back to back; L, R: DEVICE u8 [nframes][H][W];
+ * disp_out: DEVICE f32 [nframes][H][W].  Processed in chunks of the handle's
+ * max_frames, one launch sequence per chunk.  Same contract as
+ * stereo_compute (enqueued on `stream`, no synchronisation, no allocation). */
 int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
                          float* disp_out, void* stream);
 
@@ -226,17 +250,75 @@ int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb,
  * pointers or n < 0. */
 int stereo_disparity_to_depth(const float* disp, float* Z, int n, float fB, void* stream);
 
-/* Row-band support.  A band of a frame is computed by running
- * the normal pipeline on a sub-image whose halo rows cover the dependency cone
- * of the band's own rows; only rule (d) of the fill (a row without any valid
- * pixel takes the nearest valid value in raster order, which may lie in
- * another band) needs global information.  stereo_patch_rows sets the listed
- * scaled rows (HOST int32 rows[n], band-local) of D^{+L} to the HOST values[n]
- * and recomputes the scale-up rows that read them into disp_out (DEVICE, the
- * band's f32 output); L is the band's DEVICE original left image (K = 2).
- * Synchronises `stream` before returning. */
-int stereo_patch_rows(stereo_t* h, const int32_t* rows, const float* values, int n,
-                      const uint8_t* L, float* disp_out, void* stream);
+/* ---- row bands -------------------------------
+ * One frame split into horizontal bands, one per GPU.  A band owns original
+ * rows [y0_org, y0_org + rows_org) of the W x H frame.  Its handle computes
+ * SD, census, arms and C + CA_x over the band plus a halo of rows that covers
+ * the dependency cone of the own rows (Eq. 8's vertical window w_y, P:229-233;
+ * the census pattern's vertical reach; Eq. 2's pool radius; one scaled row
+ * for the cross-check/median and for Step8's odd rows),
+ * but CA + WTA only for the own scaled rows + 3 (the cross-check / median /
+ * Step8 cone) and POST only for the own rows.  Borders follow the FRAME
+ * (arms, census and Step8 see the real image edges), so the assembled bands
+ * equal the whole-frame result bit for bit.  The only frame-wide rule is fill
+ * rule (d) (reading R25b: a row with no valid pixel takes the last valid value
+ * of the nearest row above that has one, else the first of the nearest row
+ * below, else 0): it is resolved ON DEVICE from a frame-wide
+ * int32 [H/K][2] summary that the caller assembles with one element-wise MAX
+ * all-reduce (NCCL) — no host synchronisation anywhere in the band path.
+ *
+ * Per frame:  stereo_compute_band -> stereo_band_summary(summ) ->
+ *             all_reduce(summ, MAX) -> stereo_band_finish(summ), all on one
+ * stream. */
+
+/* The library's partition of a frame of H rows into nbands bands (scaled rows
+ * split as evenly as possible, band b gets rows [b*Hs/n, (b+1)*Hs/n) of the
+ * Hs = H/K scaled rows; the last band also owns the extra row of an odd H).
+ * Pure host arithmetic.  STEREO_EINVAL if nbands is not in 1..H/K or band is
+ * not in 0..nbands-1; p supplies k_scale. */
+int stereo_band_rows(int H, const stereo_params* p, int nbands, int band, int* y0_org,
+                     int* rows_org);
+
+/* Create the handle of the band [y0_org, y0_org + rows_org) of a W x H frame
+ * (same validation as stereo_create, on the frame).  y0_org must be a
+ * multiple of K and y0_org + rows_org a multiple of K or H, else
+ * STEREO_EINVAL.  Buffers are sized for the band's sub-image (own rows +
+ * halo), allocated here. */
+int stereo_create_band(int W, int H, int D, const stereo_params* p, int y0_org, int rows_org,
+                       stereo_t** out);
+
+/* Halo rows the band [y0_org, y0_org + rows_org) of a frame of H rows needs
+ * above / below its own rows (fewer at the frame's top / bottom edge), for
+ * the parameters p (k_scale, w_y, m_pool, census_dy).  Pure host arithmetic
+ * (no device needed); HOST outputs.  The same rules as stereo_create_band. */
+int stereo_band_halo(int H, const stereo_params* p, int y0_org, int rows_org, int* halo_top_org,
+                     int* halo_bot_org);
+
+/* One frame of the band.  L_band, R_band: DEVICE u8 [halo_top + rows_org +
+ * halo_bot][W], the frame's rows [y0_org - halo_top, y0_org + rows_org +
+ * halo_bot) (the caller exchanges the halo rows with the neighbouring bands).
+ * out_band: DEVICE f32 [rows_org][W], receives the band's own rows of
+ * D^{fL_org}, final unless fill rule (d) applies to one of them (see
+ * stereo_band_finish).  y0_org / rows_org / halos must equal the handle's
+ * (STEREO_EINVAL otherwise).  Enqueued on `stream`; no synchronisation. */
+int stereo_compute_band(stereo_t* h, const uint8_t* L_band, const uint8_t* R_band, int y0_org,
+                        int rows_org, int halo_top_org, int halo_bot_org, float* out_band,
+                        void* stream);
+
+/* Write the band's per-row fill summaries into summ: DEVICE int32 [H/K][2]
+ * over the whole frame, (last valid value, first valid value) of each own
+ * scaled row after the median (-1 = no valid pixel), and -1 in every other
+ * row, so that an element-wise MAX over the bands assembles the frame.
+ * Enqueued on `stream` after the band's stereo_compute_band. */
+int stereo_band_summary(stereo_t* h, int32_t* summ_dev, void* stream);
+
+/* Resolve fill rule (d) for the rows the band's output reads, from the
+ * frame-wide summ (DEVICE int32 [H/K][2], all bands assembled), and recompute
+ * Step8 for the own output rows that read a patched row.  L_band / out_band
+ * as in stereo_compute_band.  One small kernel that returns at once when no
+ * such row is all-invalid.  Enqueued on `stream`. */
+int stereo_band_finish(stereo_t* h, const int32_t* summ_dev, const uint8_t* L_band,
+                       float* out_band, void* stream);
 
 /* Per-stage device timing with CUDA events recorded on the compute stream.
  * stereo_set_timing(h, 1) resets the accumulators and starts recording around

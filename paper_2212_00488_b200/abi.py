@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("STEREO_B200_LIB", os.path.join(_HERE, "lib", "libstereo_b200.so"))
 
-STEREO_ABI_VERSION = 2
+STEREO_ABI_VERSION = 3
 STEREO_OK, STEREO_EINVAL, STEREO_ENOMEM, STEREO_ECUDA, STEREO_EUNSUPPORTED = 0, -1, -2, -3, -4
 
 (BUF_PIX_L, BUF_PIX_R, BUF_ARM_L, BUF_ARM_R, BUF_CAX_L, BUF_CAX_R, BUF_CA_L, BUF_CA_R,
@@ -38,8 +38,10 @@ EXPORTS = (
     "stereo_default_params", "stereo_create", "stereo_compute", "stereo_compute_batch",
     "stereo_compute_host", "stereo_destroy", "stereo_last_error", "stereo_get_info",
     "stereo_get_tables", "stereo_debug_download", "stereo_debug_upload", "stereo_set_debug",
-    "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms", "stereo_patch_rows",
+    "stereo_run_stage", "stereo_set_timing", "stereo_stage_times_ms",
     "stereo_rgb_to_gray", "stereo_compute_rgb", "stereo_disparity_to_depth",
+    "stereo_create_batch", "stereo_band_rows", "stereo_create_band", "stereo_band_halo",
+    "stereo_compute_band", "stereo_band_summary", "stereo_band_finish",
 )
 
 
@@ -71,6 +73,10 @@ class Info(C.Structure):
         ("device_bytes", C.c_uint64), ("cax_bytes", C.c_uint64),
         ("launches_per_frame", C.c_int32), ("ypass_block_rows", C.c_int32),
         ("cax_pitch", C.c_int32),
+        ("max_frames", C.c_int32), ("band", C.c_int32),
+        ("band_y0_org", C.c_int32), ("band_rows_org", C.c_int32),
+        ("band_halo_top_org", C.c_int32), ("band_halo_bot_org", C.c_int32),
+        ("ypass_rows", C.c_int32),
     ]
 
 
@@ -109,7 +115,15 @@ def lib():
             "stereo_run_stage": (i32, [vp, i32, vp, vp, vp, vp]),
             "stereo_set_timing": (i32, [vp, i32]),
             "stereo_stage_times_ms": (i32, [vp, vp, C.POINTER(C.c_int)]),
-            "stereo_patch_rows": (i32, [vp, vp, vp, i32, vp, vp, vp]),
+            "stereo_create_batch": (i32, [i32, i32, i32, C.POINTER(Params), i32, C.POINTER(vp)]),
+            "stereo_band_rows": (i32, [i32, C.POINTER(Params), i32, i32, C.POINTER(i32),
+                                       C.POINTER(i32)]),
+            "stereo_create_band": (i32, [i32, i32, i32, C.POINTER(Params), i32, i32, C.POINTER(vp)]),
+            "stereo_band_halo": (i32, [i32, C.POINTER(Params), i32, i32, C.POINTER(i32),
+                                       C.POINTER(i32)]),
+            "stereo_compute_band": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
+            "stereo_band_summary": (i32, [vp, vp, vp]),
+            "stereo_band_finish": (i32, [vp, vp, vp, vp, vp]),
             "stereo_rgb_to_gray": (i32, [vp, vp, i32, i32, vp]),
             "stereo_compute_rgb": (i32, [vp, vp, vp, vp, vp]),
             "stereo_disparity_to_depth": (i32, [vp, vp, i32, C.c_float, vp]),
@@ -147,10 +161,45 @@ def _ptr(t):
     if isinstance(t, int):
         return t
     if isinstance(t, np.ndarray):
-        assert t.flags["C_CONTIGUOUS"]
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
         return t.ctypes.data
-    assert t.is_contiguous(), "tensors must be contiguous"
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
     return t.data_ptr()
+
+
+_DT = {"u8": (np.uint8, "torch.uint8"), "f32": (np.float32, "torch.float32"),
+       "i32": (np.int32, "torch.int32")}
+
+
+def _dev(t, name, dtype, shape, device):
+    """A CUDA tensor on the handle's device with the given dtype and shape."""
+    if isinstance(t, int):  # raw device pointer: the caller vouches for it
+        return t
+    if isinstance(t, np.ndarray) or not getattr(t, "is_cuda", False):
+        raise ValueError(f"{name} must be a CUDA tensor on cuda:{device}")
+    if t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the handle on cuda:{device}")
+    if str(t.dtype) != _DT[dtype][1]:
+        raise ValueError(f"{name} must be {_DT[dtype][1]}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    return _ptr(t)
+
+
+def _host(a, name, dtype, shape):
+    """A host buffer (numpy array or CPU tensor) of the given dtype and shape."""
+    if isinstance(a, int):
+        return a
+    if getattr(a, "is_cuda", False):
+        raise ValueError(f"{name} must be a HOST buffer")
+    ok = (a.dtype == _DT[dtype][0]) if isinstance(a, np.ndarray) else (str(a.dtype) == _DT[dtype][1])
+    if not ok:
+        raise ValueError(f"{name} must be {dtype}, got {a.dtype}")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+    return _ptr(a)
 
 
 def _stream_ptr(stream):
@@ -168,14 +217,19 @@ def _stream_ptr(stream):
 class Stereo:
     """Owns one stereo_t handle (device-bound; not re-entrant across streams)."""
 
-    def __init__(self, W: int, H: int, D: int, params: Params | None = None, **overrides):
+    def __init__(self, W: int, H: int, D: int, params: Params | None = None,
+                 max_frames: int = 1, **overrides):
         self.params = params if params is not None else default_params(**overrides)
         h = C.c_void_p()
-        _check(lib().stereo_create(W, H, D, C.byref(self.params), C.byref(h)))
+        if max_frames == 1:
+            _check(lib().stereo_create(W, H, D, C.byref(self.params), C.byref(h)))
+        else:
+            _check(lib().stereo_create_batch(W, H, D, C.byref(self.params), max_frames, C.byref(h)))
         self._h = h
         self.info = Info()
         _check(lib().stereo_get_info(self._h, C.byref(self.info)))
         self.W, self.H, self.D = W, H, D
+        self.device = self.info.device
 
     # ------------------------------------------------------------ lifetime
     def close(self):
@@ -198,24 +252,34 @@ class Stereo:
     # ------------------------------------------------------------ compute
     def compute(self, L, R, out, stream=None):
         """L, R: CUDA u8 [H][W]; out: CUDA f32 [H][W]. Enqueued, not synchronised."""
-        _check(lib().stereo_compute(self._h, _ptr(L), _ptr(R), _ptr(out), _stream_ptr(stream)))
+        hw, d = (self.H, self.W), self.device
+        _check(lib().stereo_compute(self._h, _dev(L, "L", "u8", hw, d), _dev(R, "R", "u8", hw, d),
+                                    _dev(out, "out", "f32", hw, d), _stream_ptr(stream)))
         return out
 
     def compute_rgb(self, L_rgb, R_rgb, out, stream=None):
         """L_rgb, R_rgb: CUDA u8 [H][W][3]; gray front end (§III item 1) + pipeline."""
-        _check(lib().stereo_compute_rgb(self._h, _ptr(L_rgb), _ptr(R_rgb), _ptr(out),
+        hw3, d = (self.H, self.W, 3), self.device
+        _check(lib().stereo_compute_rgb(self._h, _dev(L_rgb, "L_rgb", "u8", hw3, d),
+                                        _dev(R_rgb, "R_rgb", "u8", hw3, d),
+                                        _dev(out, "out", "f32", (self.H, self.W), d),
                                         _stream_ptr(stream)))
         return out
 
     def compute_batch(self, L, R, out, nframes, stream=None):
-        _check(lib().stereo_compute_batch(self._h, _ptr(L), _ptr(R), nframes, _ptr(out),
+        """L, R: CUDA u8 [n][H][W]; out: CUDA f32 [n][H][W], n = nframes; one
+        launch sequence per chunk of max_frames frames."""
+        nhw, d = (nframes, self.H, self.W), self.device
+        _check(lib().stereo_compute_batch(self._h, _dev(L, "L", "u8", nhw, d), _dev(R, "R", "u8", nhw, d),
+                                          nframes, _dev(out, "out", "f32", nhw, d),
                                           _stream_ptr(stream)))
         return out
 
     def compute_host(self, L, R, out, stream=None):
         """HOST buffers (pinned for async copies); caller synchronises the stream."""
-        _check(lib().stereo_compute_host(self._h, _ptr(L), _ptr(R), _ptr(out),
-                                         _stream_ptr(stream)))
+        hw = (self.H, self.W)
+        _check(lib().stereo_compute_host(self._h, _host(L, "L", "u8", hw), _host(R, "R", "u8", hw),
+                                         _host(out, "out", "f32", hw), _stream_ptr(stream)))
         return out
 
     # ------------------------------------------------------------ debug / stages
@@ -268,12 +332,6 @@ class Stereo:
         _check(lib().stereo_run_stage(self._h, stage, _ptr(L), _ptr(R), _ptr(out),
                                       _stream_ptr(stream)))
 
-    def patch_rows(self, rows, values, L, out, stream=None):
-        rows = np.ascontiguousarray(rows, dtype=np.int32)
-        values = np.ascontiguousarray(values, dtype=np.float32)
-        _check(lib().stereo_patch_rows(self._h, rows.ctypes.data, values.ctypes.data, len(rows),
-                                       _ptr(L), _ptr(out), _stream_ptr(stream)))
-
     def set_timing(self, enable=True):
         _check(lib().stereo_set_timing(self._h, int(enable)))
 
@@ -282,6 +340,86 @@ class Stereo:
         n = C.c_int()
         _check(lib().stereo_stage_times_ms(self._h, ms.ctypes.data, C.byref(n)))
         return dict(zip(STAGE_NAMES, ms.tolist())), n.value
+
+
+def band_rows(H, nbands, band, params: Params | None = None, **overrides):
+    """The library's band partition: (y0_org, rows_org) of band `band`."""
+    p = params if params is not None else default_params(**overrides)
+    y0, rows = C.c_int(), C.c_int()
+    _check(lib().stereo_band_rows(H, C.byref(p), nbands, band, C.byref(y0), C.byref(rows)))
+    return y0.value, rows.value
+
+
+def band_halo(H, y0_org, rows_org, params: Params | None = None, **overrides):
+    """Halo rows (above, below) the band needs (stereo_band_halo; host only)."""
+    p = params if params is not None else default_params(**overrides)
+    top, bot = C.c_int(), C.c_int()
+    _check(lib().stereo_band_halo(H, C.byref(p), y0_org, rows_org, C.byref(top), C.byref(bot)))
+    return top.value, bot.value
+
+
+class StereoBand:
+    """A row-band handle (stereo_create_band): own original rows
+    [y0_org, y0_org + rows_org) of a W x H frame, computed from the band plus
+    the halo rows stereo_band_halo names; see include/stereo.h."""
+
+    def __init__(self, W, H, D, y0_org, rows_org, params: Params | None = None, **overrides):
+        self.params = params if params is not None else default_params(**overrides)
+        h = C.c_void_p()
+        _check(lib().stereo_create_band(W, H, D, C.byref(self.params), y0_org, rows_org,
+                                        C.byref(h)))
+        self._h = h
+        self.info = Info()
+        _check(lib().stereo_get_info(self._h, C.byref(self.info)))
+        self.W, self.H, self.D = W, H, D
+        self.y0, self.rows = y0_org, rows_org
+        self.top, self.bot = self.info.band_halo_top_org, self.info.band_halo_bot_org
+        self.sub_rows = self.top + self.rows + self.bot  # rows of L_band / R_band
+        self.sub_y0 = y0_org - self.top                   # frame row of L_band[0]
+        self.Hs = H // self.params.k_scale
+        self.device = self.info.device
+
+    def compute(self, L_band, R_band, out_band, stream=None):
+        """L_band, R_band: CUDA u8 [sub_rows][W]; out_band: CUDA f32 [rows][W]."""
+        d, sh = self.device, (self.sub_rows, self.W)
+        _check(lib().stereo_compute_band(self._h, _dev(L_band, "L_band", "u8", sh, d),
+                                         _dev(R_band, "R_band", "u8", sh, d), self.y0, self.rows,
+                                         self.top, self.bot,
+                                         _dev(out_band, "out_band", "f32", (self.rows, self.W), d),
+                                         _stream_ptr(stream)))
+        return out_band
+
+    def summary(self, summ, stream=None):
+        """summ: CUDA int32 [H/K][2] (frame-wide; own rows written, -1 elsewhere)."""
+        _check(lib().stereo_band_summary(self._h, _dev(summ, "summ", "i32", (self.Hs, 2), self.device),
+                                         _stream_ptr(stream)))
+        return summ
+
+    def finish(self, summ, L_band, out_band, stream=None):
+        """Fill rule (d) from the frame-wide summaries (all bands assembled)."""
+        d = self.device
+        _check(lib().stereo_band_finish(self._h, _dev(summ, "summ", "i32", (self.Hs, 2), d),
+                                        _dev(L_band, "L_band", "u8", (self.sub_rows, self.W), d),
+                                        _dev(out_band, "out_band", "f32", (self.rows, self.W), d),
+                                        _stream_ptr(stream)))
+        return out_band
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().stereo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def unpack_pix(pix):

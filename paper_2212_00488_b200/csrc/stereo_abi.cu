@@ -3,8 +3,10 @@
 // Owns validation (SPEC S:59-61 order), the fixed-point table builder, the
 // buffer planner, the per-frame launch sequence (Step1..Step8 order)
 // and the CUDA-event stage timers.  No kernel runs at create time.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -40,6 +42,20 @@ struct TimedFrame {
   cudaEvent_t ev[STEREO_STAGE_COUNT + 1];
   int stage[STEREO_STAGE_COUNT];
   int n;
+  int frames;  // frames of this launch sequence (a batch chunk)
+};
+
+// Entry points run on the handle's device whatever the calling thread's
+// current device is (buffers, tensor maps and planned attributes live there).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 }  // namespace
 
@@ -53,6 +69,7 @@ struct stereo_s {
   uint32_t qad_h[256];
   uint32_t qmc_h[7];
   std::vector<void*> allocs;
+  uint64_t bytes = 0;  // device bytes owned (every allocation, padding included)
   // timing
   bool timing = false;
   std::vector<TimedFrame> pending;
@@ -69,6 +86,7 @@ int alloc(stereo_t* h, void** p, size_t bytes) {
   if (e != cudaSuccess)
     return fail(STEREO_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
   h->allocs.push_back(*p);
+  h->bytes += bytes;
   // defined contents from the start: the tail paddings that the word loads of
   // PREP / POST over-read are then initialised (compute-sanitizer initcheck)
   e = cudaMemset(*p, 0, bytes);
@@ -154,15 +172,18 @@ int drain_one(stereo_t* h, size_t idx) {
     h->acc_ms[f.stage[i]] += ms;
   }
   for (int i = 0; i <= f.n; ++i) h->pool.push_back(f.ev[i]);
-  h->acc_frames += 1;
+  h->acc_frames += f.frames;
   return STEREO_OK;
 }
 
-// One frame: the Step1..Step8 launch sequence.
-int enqueue_frame(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, cudaStream_t s) {
+// nfr frames (1..NB, back to back in L, R, out): the Step1..Step8 launch
+// sequence, each kernel launched ONCE for all nfr frames.
+int enqueue_frames(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, int nfr,
+                   cudaStream_t s) {
   const Geom& g = h->g;
   Buffers& b = h->b;
   TimedFrame tf{};
+  tf.frames = nfr;
   if (h->timing) {
     tf.ev[0] = get_event(h);
     cudaEventRecord(tf.ev[0], s);
@@ -177,19 +198,19 @@ int enqueue_frame(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, c
   const uint8_t* Ls = L;
   const uint8_t* Rs = R;
   if (g.K == 2) {
-    CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, s));
+    CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, nfr, s));
     mark(STEREO_STAGE_SD);
     Ls = b.Ls;
     Rs = b.Rs;
   }
   const bool padded = (Ls == b.Ls && Rs == b.Rs) || (Ls == b.grayL && Rs == b.grayR);
-  CU(launch_prep(g, h->plan, Ls, Rs, padded, b, s));
+  CU(launch_prep(g, h->plan, Ls, Rs, padded, b, nfr, s));
   mark(STEREO_STAGE_PREP);
-  CU(launch_xpass(g, h->plan, b, s));
+  CU(launch_xpass(g, h->plan, b, nfr, s));
   mark(STEREO_STAGE_XPASS);
-  CU(launch_ypass(g, h->plan, b, h->debug_ca, s));
+  CU(launch_ypass(g, h->plan, b, h->debug_ca, nfr, s));
   mark(STEREO_STAGE_YPASS);
-  CU(launch_post(g, h->plan, b, L, out, s));
+  CU(launch_post(g, h->plan, b, L, out, nfr, s));
   mark(STEREO_STAGE_POST);
   if (h->timing) {
     h->pending.push_back(tf);
@@ -257,18 +278,60 @@ void stereo_default_params(stereo_params* p) {
 
 const char* stereo_last_error(void) { return g_err.c_str(); }
 
-int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
-  g_err.clear();
-  if (!out) return fail(STEREO_EINVAL, "out must not be NULL");
-  *out = nullptr;
-  int rc = validate(W, H, D, p);
-  if (rc) return rc;
+}  // extern "C"
+
+namespace {
+
+// Band geometry: the sub-image of original rows
+// [r0, r1) whose own scaled rows [ys0, ys1) come out exactly as in the whole
+// frame.  The dependency cone, in scaled rows: POST's own rows read D^L / D^R
+// rows [ys0 - 1, ys1 + 1 + (K == 2)) (median +-1, Step8's odd rows read fill
+// row y + 1); those maps read CA_x rows +-w_y (Eq. 8) and the y arms of their
+// own rows (<= w_y rows away); CA_x rows read census rows +-cy (the pattern's
+// vertical reach); Eq. 2 reads original rows 2y - m .. 2y + m.
+struct BandGeom {
+  int ys0, ys1, ya, yb, sa, sb, r0, r1;
+};
+
+int band_geom(int H, const stereo_params* p, int y0_org, int rows_org, BandGeom& bg) {
+  const int K = p->k_scale, Hs = H / K;
+  int cy = 0;
+  for (int i = 0; i < 6; ++i) cy = std::max(cy, std::abs((int)p->census_dy[i]));
+  if (y0_org < 0 || rows_org < 1 || y0_org + rows_org > H)
+    return fail(STEREO_EINVAL, "band rows [%d, %d) outside the frame's %d rows", y0_org,
+                y0_org + rows_org, H);
+  const int end = y0_org + rows_org;
+  if (y0_org % K || (end % K && end != H))
+    return fail(STEREO_EINVAL, "band rows must start and end on multiples of K=%d (or end at H)", K);
+  bg.ys0 = y0_org / K;
+  bg.ys1 = end == H ? Hs : end / K;
+  if (bg.ys1 <= bg.ys0 || bg.ys0 >= Hs)
+    return fail(STEREO_EINVAL, "band [%d, %d) holds no scaled row", y0_org, end);
+  bg.ya = std::max(0, bg.ys0 - 1);
+  bg.yb = std::min(Hs, bg.ys1 + 1 + (K == 2 ? 1 : 0));
+  bg.sa = std::max(0, bg.ya - p->w_y - cy);
+  bg.sb = std::min(Hs, bg.yb + p->w_y + cy);
+  if (K == 2) {
+    bg.r0 = std::max(0, 2 * bg.sa - p->m_pool);
+    bg.r0 -= bg.r0 & 1;  // even: the scaled grids coincide
+    bg.r1 = bg.sb == Hs ? H : std::min(H, std::max(2 * (bg.sb - 1) + p->m_pool + 1, 2 * bg.sb));
+  } else {
+    bg.r0 = bg.sa;
+    bg.r1 = bg.sb == Hs ? H : bg.sb;
+  }
+  return STEREO_OK;
+}
+
+int create_impl(int W, int H, int D, const stereo_params* p, int nb, const BandGeom* bg,
+                int Hframe, int y0_org, int rows_org, stereo_t** out) {
   stereo_t* h = new (std::nothrow) stereo_t();
   if (!h) return fail(STEREO_ENOMEM, "host allocation failed");
+  int rc;
   h->params = *p;
   Geom& g = h->g;
   g.W = W; g.H = H; g.D = D; g.K = p->k_scale; g.m_pool = p->m_pool;
   g.Ws = W / g.K; g.Hs = H / g.K; g.Ds = (D + g.K - 1) / g.K;
+  g.NB = nb;
   g.Wp = 32 * xpass_chunk_for(g.Ws);  // CA_x pitch = the x pass's lane-chunk span
   g.w_x = p->w_x; g.w_y = p->w_y; g.delta = p->delta; g.t_fill = p->t_fill;
   g.w_x_r = p->w_x_r < 0 ? p->w_x : p->w_x_r;
@@ -277,6 +340,16 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
   g.f = frac_bits(g.w_x_max);
   g.border = 1u << (g.f + 1);
   for (int i = 0; i < 6; ++i) { g.cdx[i] = p->census_dx[i]; g.cdy[i] = p->census_dy[i]; }
+  if (bg) {
+    g.band = true;
+    g.H_g = Hframe;
+    g.Hs_g = Hframe / g.K;
+    g.s0 = bg->r0 / g.K;
+    g.pa = bg->ys0 - g.s0; g.pb = bg->ys1 - g.s0;
+    g.ya = bg->ya - g.s0; g.yb = bg->yb - g.s0;
+    g.y0_org = y0_org; g.rows_org = rows_org;
+    g.top = y0_org - bg->r0; g.bot = bg->r1 - (y0_org + rows_org);
+  }
   if (!xpass_chunk_for(g.Ws)) {
     delete h;
     return fail(STEREO_EUNSUPPORTED, "scaled width %d exceeds 2016", g.Ws);
@@ -291,21 +364,22 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
     return fail(STEREO_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
   }
   build_tables(*p, g.f, h->qad_h, h->qmc_h);
-  const size_t n = (size_t)g.Ws * g.Hs;
-  const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
+  const size_t n = (size_t)g.Ws * g.Hs * nb;  // per-frame buffers x NB frames
+  const size_t N = (size_t)W * H * nb;
+  const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * nb * g.Wp;  // disparity pairs (u32 x 2)
   Buffers& b = h->b;
   struct A { void** p; size_t bytes; } as[] = {
       {(void**)&b.pixL, n * 2 + 16}, {(void**)&b.pixR, n * 2 + 16}, {(void**)&b.armL, n * 4},
       {(void**)&b.armR, n * 4}, {(void**)&b.caxL, vol * 4}, {(void**)&b.caxR, vol * 4},
-      {(void**)&b.xrow, (size_t)4 * g.Hs * g.Wp * 4},
+      {(void**)&b.xrow, (size_t)4 * g.Hs * nb * g.Wp * 4},
       {(void**)&b.grayL, (size_t)W * H + 16}, {(void**)&b.grayR, (size_t)W * H + 16},
       {(void**)&b.DL, n + 16}, {(void**)&b.DR, n + 16}, {(void**)&b.masked, n}, {(void**)&b.median, n},
-      {(void**)&b.rowFirst, (size_t)g.Hs * 16}, {(void**)&b.patchRows, (size_t)g.Hs * 4},
-      {(void**)&b.patchVals, (size_t)g.Hs * 4},
-      {(void**)&b.counter, 16},
+      {(void**)&b.rowFirst, (size_t)g.Hs * 16 * nb},
+      {(void**)&b.counter, (size_t)4 * nb + 16},
       {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
       {(void**)&b.qtab, (size_t)(256 + 64) * 32 * 4},
   };
+  (void)N;
   for (auto& a : as) {
     if ((rc = alloc(h, a.p, a.bytes))) { stereo_destroy(h); return rc; }
   }
@@ -316,9 +390,7 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
       return rc;
     }
   }
-  b.rowLast = b.rowFirst + g.Hs;
-  e = cudaMemset(b.counter, 0, 16);
-  if (e == cudaSuccess) e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
+  e = cudaMemcpy(b.qad, h->qad_h, sizeof h->qad_h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(b.qmc, h->qmc_h, sizeof h->qmc_h, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {  // the x pass's shared-memory table image (one copy per bank)
     std::vector<uint32_t> tab((256 + 64) * 32);
@@ -332,6 +404,67 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
     return fail(STEREO_ECUDA, "setup: %s", cudaGetErrorString(e));
   }
   *out = h;
+  return STEREO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out) {
+  return stereo_create_batch(W, H, D, p, 1, out);
+}
+
+int stereo_create_batch(int W, int H, int D, const stereo_params* p, int max_frames,
+                        stereo_t** out) {
+  g_err.clear();
+  if (!out) return fail(STEREO_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  int rc = validate(W, H, D, p);
+  if (rc) return rc;
+  if (max_frames < 1) return fail(STEREO_EINVAL, "max_frames must be >= 1");
+  if ((size_t)max_frames * (H / p->k_scale) > (1u << 20))
+    return fail(STEREO_EUNSUPPORTED, "max_frames * H/K must be <= 2^20 rows");
+  return create_impl(W, H, D, p, max_frames, nullptr, 0, 0, 0, out);
+}
+
+int stereo_band_rows(int H, const stereo_params* p, int nbands, int band, int* y0_org,
+                     int* rows_org) {
+  g_err.clear();
+  if (!p || !y0_org || !rows_org) return fail(STEREO_EINVAL, "NULL argument");
+  if (p->k_scale < 1 || p->k_scale > 2) return fail(STEREO_EUNSUPPORTED, "k_scale must be 1 or 2");
+  const int K = p->k_scale, Hs = H / K;
+  if (H < 1 || nbands < 1 || nbands > Hs || band < 0 || band >= nbands)
+    return fail(STEREO_EINVAL, "cannot split %d scaled rows into %d bands (band %d)", Hs, nbands, band);
+  const int ys0 = (int)((long long)band * Hs / nbands), ys1 = (int)((long long)(band + 1) * Hs / nbands);
+  *y0_org = K * ys0;
+  *rows_org = (ys1 == Hs ? H : K * ys1) - K * ys0;
+  return STEREO_OK;
+}
+
+int stereo_create_band(int W, int H, int D, const stereo_params* p, int y0_org, int rows_org,
+                       stereo_t** out) {
+  g_err.clear();
+  if (!out) return fail(STEREO_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  int rc = validate(W, H, D, p);
+  if (rc) return rc;
+  BandGeom bg;
+  if ((rc = band_geom(H, p, y0_org, rows_org, bg))) return rc;
+  return create_impl(W, bg.r1 - bg.r0, D, p, 1, &bg, H, y0_org, rows_org, out);
+}
+
+int stereo_band_halo(int H, const stereo_params* p, int y0_org, int rows_org, int* halo_top_org,
+                     int* halo_bot_org) {
+  g_err.clear();
+  if (!p || !halo_top_org || !halo_bot_org) return fail(STEREO_EINVAL, "NULL argument");
+  if (p->k_scale < 1 || p->k_scale > 2) return fail(STEREO_EUNSUPPORTED, "k_scale must be 1 or 2");
+  if (p->w_y < 0 || p->m_pool < 0) return fail(STEREO_EINVAL, "w_y and m_pool must be >= 0");
+  BandGeom bg;
+  int rc = band_geom(H, p, y0_org, rows_org, bg);
+  if (rc) return rc;
+  *halo_top_org = y0_org - bg.r0;
+  *halo_bot_org = bg.r1 - (y0_org + rows_org);
   return STEREO_OK;
 }
 
@@ -354,7 +487,9 @@ void stereo_destroy(stereo_t* h) {
 int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                    void* stream) {
   if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
-  return enqueue_frame(h, L, R, disp_out, (cudaStream_t)stream);
+  if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
+  DeviceGuard dg(h->device);
+  return enqueue_frames(h, L, R, disp_out, 1, (cudaStream_t)stream);
 }
 
 int stereo_rgb_to_gray(const uint8_t* rgb, uint8_t* gray, int W, int H, void* stream) {
@@ -376,18 +511,24 @@ int stereo_disparity_to_depth(const float* disp, float* Z, int n, float fB, void
 int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb, float* disp_out,
                        void* stream) {
   if (!h || !L_rgb || !R_rgb || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
+  DeviceGuard dg(h->device);
   const cudaStream_t s = (cudaStream_t)stream;
   CU(launch_gray(L_rgb, R_rgb, h->b.grayL, h->b.grayR, h->g.W, h->g.H, s));
-  return enqueue_frame(h, h->b.grayL, h->b.grayR, disp_out, s);
+  return enqueue_frames(h, h->b.grayL, h->b.grayR, disp_out, 1, s);
 }
 
 int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
                          float* disp_out, void* stream) {
   if (!h || !L || !R || !disp_out || nframes < 0)
     return fail(STEREO_EINVAL, "NULL handle/buffer or negative nframes");
+  if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
+  DeviceGuard dg(h->device);
   const size_t in = (size_t)h->g.W * h->g.H;
-  for (int i = 0; i < nframes; ++i) {
-    int rc = enqueue_frame(h, L + i * in, R + i * in, disp_out + i * in, (cudaStream_t)stream);
+  // chunks of NB frames: five launches per chunk, whatever the chunk size
+  for (int i = 0; i < nframes; i += h->g.NB) {
+    const int nfr = std::min(h->g.NB, nframes - i);
+    int rc = enqueue_frames(h, L + i * in, R + i * in, disp_out + i * in, nfr, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return STEREO_OK;
@@ -396,6 +537,8 @@ int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nf
 int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                         void* stream) {
   if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
+  DeviceGuard dg(h->device);
   const size_t in = (size_t)h->g.W * h->g.H;
   int rc;
   if (!h->b.inL) {
@@ -406,7 +549,7 @@ int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* 
   cudaStream_t s = (cudaStream_t)stream;
   CU(cudaMemcpyAsync(h->b.inL, L, in, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->b.inR, R, in, cudaMemcpyHostToDevice, s));
-  if ((rc = enqueue_frame(h, h->b.inL, h->b.inR, h->b.outF, s))) return rc;
+  if ((rc = enqueue_frames(h, h->b.inL, h->b.inR, h->b.outF, 1, s))) return rc;
   CU(cudaMemcpyAsync(disp_out, h->b.outF, in * 4, cudaMemcpyDeviceToHost, s));
   return STEREO_OK;
 }
@@ -418,16 +561,19 @@ int stereo_get_info(const stereo_t* h, stereo_info* info) {
   info->Ws = g.Ws; info->Hs = g.Hs; info->Ds = g.Ds;
   info->frac_bits = g.f;
   info->device = h->device;
-  uint64_t tot = 0;
-  const size_t n = (size_t)g.Ws * g.Hs;
   const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
-  tot += n * (2 + 2 + 4 + 4 + 1 + 1 + 1 + 1 + 4) + vol * 8 + (size_t)g.Hs * 8 + 263 * 4;
-  if (g.K == 2) tot += 2 * n;
-  info->device_bytes = tot;
+  info->device_bytes = h->bytes + (h->b.caL ? 2 * (size_t)g.Ds * g.Hs * g.Ws * 8 : 0);
   info->cax_bytes = vol * 4;
   info->launches_per_frame = g.K == 2 ? 5 : 4;
   info->ypass_block_rows = h->plan.ypass_B;
   info->cax_pitch = g.Wp;
+  info->max_frames = g.NB;
+  info->band = g.band ? 1 : 0;
+  info->band_y0_org = g.y0_org;
+  info->band_rows_org = g.rows_org;
+  info->band_halo_top_org = g.top;
+  info->band_halo_bot_org = g.bot;
+  info->ypass_rows = g.band ? g.yb - g.ya : g.Hs;
   return STEREO_OK;
 }
 
@@ -441,6 +587,8 @@ int stereo_get_tables(const stereo_t* h, uint32_t* qad, uint32_t* qmc, uint32_t*
 
 int stereo_debug_download(stereo_t* h, int buf_id, void* host_dst, size_t bytes) {
   if (!h || !host_dst) return fail(STEREO_EINVAL, "NULL argument");
+  if (h->g.NB != 1) return fail(STEREO_EINVAL, "stage access needs a handle of batch capacity 1");
+  DeviceGuard dg(h->device);
   BufView v = buf_view(h, buf_id);
   if (!v.p) return fail(STEREO_EINVAL, "buffer %d not available", buf_id);
   if (bytes != v.bytes) return fail(STEREO_EINVAL, "buffer %d has %zu bytes, not %zu", buf_id, v.bytes, bytes);
@@ -451,6 +599,8 @@ int stereo_debug_download(stereo_t* h, int buf_id, void* host_dst, size_t bytes)
 
 int stereo_debug_upload(stereo_t* h, int buf_id, const void* host_src, size_t bytes) {
   if (!h || !host_src) return fail(STEREO_EINVAL, "NULL argument");
+  if (h->g.NB != 1) return fail(STEREO_EINVAL, "stage access needs a handle of batch capacity 1");
+  DeviceGuard dg(h->device);
   BufView v = buf_view(h, buf_id);
   if (!v.p) return fail(STEREO_EINVAL, "buffer %d not available", buf_id);
   if (bytes != v.bytes) return fail(STEREO_EINVAL, "buffer %d has %zu bytes, not %zu", buf_id, v.bytes, bytes);
@@ -462,6 +612,8 @@ int stereo_debug_upload(stereo_t* h, int buf_id, const void* host_src, size_t by
 int stereo_set_debug(stereo_t* h, int what, int enable) {
   if (!h) return fail(STEREO_EINVAL, "NULL handle");
   if (what != STEREO_DEBUG_CA) return fail(STEREO_EINVAL, "unknown debug switch %d", what);
+  if (h->g.NB != 1) return fail(STEREO_EINVAL, "stage access needs a handle of batch capacity 1");
+  DeviceGuard dg(h->device);
   if (enable && !h->b.caL) {
     const size_t bytes = (size_t)h->g.Ds * h->g.Hs * h->g.Ws * 8;
     CU(cudaMalloc(&h->b.caL, bytes));
@@ -474,6 +626,8 @@ int stereo_set_debug(stereo_t* h, int what, int enable) {
 int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t* R,
                      float* disp_out, void* stream) {
   if (!h) return fail(STEREO_EINVAL, "NULL handle");
+  if (h->g.NB != 1) return fail(STEREO_EINVAL, "stage access needs a handle of batch capacity 1");
+  DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const Geom& g = h->g;
   Buffers& b = h->b;
@@ -481,41 +635,57 @@ int stereo_run_stage(stereo_t* h, int stage_id, const uint8_t* L, const uint8_t*
     case STEREO_STAGE_SD:
       if (g.K == 2) {
         if (!L || !R) return fail(STEREO_EINVAL, "SD needs L and R");
-        CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, s));
+        CU(launch_sd(g, h->plan, L, R, b.Ls, b.Rs, 1, s));
       }
       return STEREO_OK;
     case STEREO_STAGE_PREP:
       if (g.K == 1 && (!L || !R)) return fail(STEREO_EINVAL, "PREP with K=1 needs L and R");
-      CU(launch_prep(g, h->plan, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, g.K == 2, b, s));
+      CU(launch_prep(g, h->plan, g.K == 2 ? b.Ls : L, g.K == 2 ? b.Rs : R, g.K == 2, b, 1, s));
       return STEREO_OK;
-    case STEREO_STAGE_XPASS: CU(launch_xpass(g, h->plan, b, s)); return STEREO_OK;
-    case STEREO_STAGE_YPASS: CU(launch_ypass(g, h->plan, b, h->debug_ca, s)); return STEREO_OK;
+    case STEREO_STAGE_XPASS: CU(launch_xpass(g, h->plan, b, 1, s)); return STEREO_OK;
+    case STEREO_STAGE_YPASS: CU(launch_ypass(g, h->plan, b, h->debug_ca, 1, s)); return STEREO_OK;
     case STEREO_STAGE_POST:
       if (!disp_out || (g.K == 2 && !L)) return fail(STEREO_EINVAL, "POST needs disp_out (and L when K=2)");
-      CU(launch_post(g, h->plan, b, L, disp_out, s));
+      CU(launch_post(g, h->plan, b, L, disp_out, 1, s));
       return STEREO_OK;
     default: return fail(STEREO_EINVAL, "unknown stage %d", stage_id);
   }
 }
 
-int stereo_patch_rows(stereo_t* h, const int32_t* rows, const float* values, int n,
-                      const uint8_t* L, float* disp_out, void* stream) {
-  if (!h || n < 0 || (n > 0 && (!rows || !values || !disp_out)) || (h->g.K == 2 && n > 0 && !L))
-    return fail(STEREO_EINVAL, "invalid patch arguments");
-  if (n > h->g.Hs) return fail(STEREO_EINVAL, "more rows than the handle has");
-  for (int i = 0; i < n; ++i)
-    if (rows[i] < 0 || rows[i] >= h->g.Hs) return fail(STEREO_EINVAL, "patch row %d out of range", rows[i]);
-  if (n == 0) return STEREO_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(h->b.patchRows, rows, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(h->b.patchVals, values, sizeof(float) * n, cudaMemcpyHostToDevice, s));
-  CU(launch_patch(h->g, h->b, L, disp_out, h->b.patchRows, h->b.patchVals, n, s));
-  CU(cudaStreamSynchronize(s));  // rows/values are caller-owned host memory
+int stereo_compute_band(stereo_t* h, const uint8_t* L_band, const uint8_t* R_band, int y0_org,
+                        int rows_org, int halo_top_org, int halo_bot_org, float* out_band,
+                        void* stream) {
+  if (!h || !L_band || !R_band || !out_band) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  const Geom& g = h->g;
+  if (!g.band) return fail(STEREO_EINVAL, "not a band handle (stereo_create_band)");
+  if (y0_org != g.y0_org || rows_org != g.rows_org || halo_top_org != g.top || halo_bot_org != g.bot)
+    return fail(STEREO_EINVAL,
+                "band (y0 %d, rows %d, halo %d/%d) differs from the handle's (y0 %d, rows %d, halo %d/%d)",
+                y0_org, rows_org, halo_top_org, halo_bot_org, g.y0_org, g.rows_org, g.top, g.bot);
+  DeviceGuard dg(h->device);
+  return enqueue_frames(h, L_band, R_band, out_band, 1, (cudaStream_t)stream);
+}
+
+int stereo_band_summary(stereo_t* h, int32_t* summ_dev, void* stream) {
+  if (!h || !summ_dev) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  if (!h->g.band) return fail(STEREO_EINVAL, "not a band handle (stereo_create_band)");
+  DeviceGuard dg(h->device);
+  CU(launch_band_summary(h->g, h->b, summ_dev, (cudaStream_t)stream));
+  return STEREO_OK;
+}
+
+int stereo_band_finish(stereo_t* h, const int32_t* summ_dev, const uint8_t* L_band,
+                       float* out_band, void* stream) {
+  if (!h || !summ_dev || !L_band || !out_band) return fail(STEREO_EINVAL, "NULL handle or buffer");
+  if (!h->g.band) return fail(STEREO_EINVAL, "not a band handle (stereo_create_band)");
+  DeviceGuard dg(h->device);
+  CU(launch_band_finish(h->g, h->b, summ_dev, L_band, out_band, (cudaStream_t)stream));
   return STEREO_OK;
 }
 
 int stereo_set_timing(stereo_t* h, int enable) {
   if (!h) return fail(STEREO_EINVAL, "NULL handle");
+  DeviceGuard dg(h->device);
   for (size_t i = 0; i < h->pending.size(); ++i) {
     cudaEventSynchronize(h->pending[i].ev[h->pending[i].n]);
     for (int k = 0; k <= h->pending[i].n; ++k) h->pool.push_back(h->pending[i].ev[k]);
@@ -535,6 +705,7 @@ int stereo_set_timing(stereo_t* h, int enable) {
 
 int stereo_stage_times_ms(stereo_t* h, double* ms, int* nframes) {
   if (!h || !ms) return fail(STEREO_EINVAL, "NULL argument");
+  DeviceGuard dg(h->device);
   for (size_t i = 0; i < h->pending.size(); ++i) {
     int rc = drain_one(h, i);
     if (rc) return rc;

@@ -22,6 +22,20 @@ struct Geom {
   int f;            // fixed-point fraction bits
   uint32_t border;  // 2^(f+1): the BORDER cost (reading R12b)
   int8_t cdx[6], cdy[6];
+  // frame batch: buffers hold NB frames; one launch of every kernel serves up
+  // to NB frames (SD / PREP / POST index the frame by blockIdx.z; the x and
+  // y passes see the batch as one image of NB*Hs rows: both are row-local or
+  // window-local, and no window crosses a frame border since the arms stop at
+  // the frame's own borders)
+  int NB = 1;
+  // row-band mode (stereo_create_band; W x H above is then the band's
+  // sub-image: own rows + halo): own scaled rows [pa, pb) and the rows whose
+  // D^L / D^R POST reads, [ya, yb), in sub-image coordinates; s0 = global
+  // scaled row of sub-image row 0; Hs_g = the frame's scaled height
+  bool band = false;
+  int pa = 0, pb = 0, ya = 0, yb = 0;
+  int s0 = 0, Hs_g = 0, H_g = 0;
+  int y0_org = 0, rows_org = 0, top = 0, bot = 0;  // own original rows, halo rows
 };
 
 // Device buffers owned by a handle.
@@ -42,11 +56,8 @@ struct Buffers {
   uint8_t* DR = nullptr;
   uint8_t* masked = nullptr;
   uint8_t* median = nullptr;
-  int32_t* rowFirst = nullptr;  // int32 [4][Hs]: first valid x, last valid x, their values (-1 = none)
-  int32_t* rowLast = nullptr;   // = rowFirst + Hs
-  int32_t* patchRows = nullptr; // rule-(d) patch scratch: int32 [Hs] rows + f32 [Hs] values
-  float* patchVals = nullptr;
-  unsigned* counter = nullptr;  // POST last-block counter (self-resetting)
+  int32_t* rowFirst = nullptr;  // int32 [NB][4][Hs]: first valid x, last valid x, their values (-1 = none)
+  unsigned* counter = nullptr;  // POST last-block counters, one per frame (self-resetting)
   float* fill = nullptr;        // f32 [Hs][Ws]
   uint32_t* qad = nullptr;      // u32 [256]
   uint32_t* qmc = nullptr;      // u32 [7]
@@ -82,22 +93,30 @@ struct Plan {
   int prep_rows = 1;  // pixel rows per PREP thread (tile 32 x 8*prep_rows)
 };
 
-// Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch error.
+// Launchers (stereo_kernels.cu).  All enqueue on `s` and return the launch
+// error.  nfr = frames of this launch (1..g.NB), stored at frame slots 0..nfr-1
+// of the handle's buffers; Lorg / Rorg / out hold nfr frames back to back.
 cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const uint8_t* Rorg,
-                      uint8_t* Ls, uint8_t* Rs, cudaStream_t s);
+                      uint8_t* Ls, uint8_t* Rs, int nfr, cudaStream_t s);
 // padded: Ls / Rs are handle buffers with >= 3 bytes of tail padding (word loads)
 cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs, bool padded,
-                        Buffers& b, cudaStream_t s);
-cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s);
-cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
+                        Buffers& b, int nfr, cudaStream_t s);
+cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, int nfr, cudaStream_t s);
+cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca, int nfr,
                          cudaStream_t s);
+// band mode: out = the caller's band output (own original rows only)
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
-                        float* out, cudaStream_t s);
+                        float* out, int nfr, cudaStream_t s);
 cudaError_t launch_depth(const float* disp, float* Z, int n, float fB, cudaStream_t s);
 cudaError_t launch_gray(const uint8_t* rgb0, const uint8_t* rgb1, uint8_t* g0, uint8_t* g1,
                         int W, int H, cudaStream_t s);
-cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,
-                         const int32_t* rows_dev, const float* vals_dev, int n, cudaStream_t s);
+// band mode: own-row summaries into the frame-wide int32 [Hs_g][2] buffer
+// (last valid value, first valid value; -1 elsewhere) / rule (d) from the
+// frame-wide summaries, then Step8 again for the output rows that read a
+// patched row (a no-op kernel when the band has no all-invalid row)
+cudaError_t launch_band_summary(const Geom& g, Buffers& b, int32_t* summ, cudaStream_t s);
+cudaError_t launch_band_finish(const Geom& g, Buffers& b, const int32_t* summ,
+                               const uint8_t* Lorg, float* out, cudaStream_t s);
 
 // Plan helpers
 int xpass_chunk_for(int Ws);  // 0 if unsupported

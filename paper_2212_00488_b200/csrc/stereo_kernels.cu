@@ -15,17 +15,10 @@
 #include <cstdlib>
 
 #include <algorithm>
-#include "stereo_internal.cuh"
+#include "stereo_common.cuh"
 
 namespace stereo {
 
-namespace {
-constexpr unsigned kFull = 0xffffffffu;
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-}  // namespace
 
 // ============================================================================
 // SD — Eq. 2, Step1: L(x,y) = mean of the (2m+1)^2
@@ -38,12 +31,13 @@ __global__ void __launch_bounds__(256) sd_kernel(const uint8_t* __restrict__ Lor
                                                  const uint8_t* __restrict__ Rorg,
                                                  uint8_t* __restrict__ Ls,
                                                  uint8_t* __restrict__ Rs, int W, int H,
-                                                 int Ws) {
+                                                 int Ws, int Hs) {
   extern __shared__ uint32_t sdm32[];
   uint8_t* sdm = reinterpret_cast<uint8_t*>(sdm32);
   constexpr int NR = 2 * M + 1, N = NR * NR;
-  const uint8_t* src = blockIdx.y ? Rorg : Lorg;
-  uint8_t* dst = blockIdx.y ? Rs : Ls;
+  // blockIdx.z: frame of the batch (frames back to back in both buffers)
+  const uint8_t* src = (blockIdx.y ? Rorg : Lorg) + (size_t)blockIdx.z * W * H;
+  uint8_t* dst = (blockIdx.y ? Rs : Ls) + (size_t)blockIdx.z * Ws * Hs;
   const int y = blockIdx.x;
   const int Wq = (W + 3) & ~3;
   const bool vec = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(src) & 3) == 0);
@@ -100,13 +94,13 @@ __global__ void __launch_bounds__(256) sd_kernel(const uint8_t* __restrict__ Lor
 }
 
 cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const uint8_t* Rorg,
-                      uint8_t* Ls, uint8_t* Rs, cudaStream_t s) {
-  dim3 grid(g.Hs, 2);
+                      uint8_t* Ls, uint8_t* Rs, int nfr, cudaStream_t s) {
+  dim3 grid(g.Hs, 2, nfr);
   switch (g.m_pool) {
-    case 0: sd_kernel<0><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
-    case 1: sd_kernel<1><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
-    case 2: sd_kernel<2><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
-    default: sd_kernel<3><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws); break;
+    case 0: sd_kernel<0><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws, g.Hs); break;
+    case 1: sd_kernel<1><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws, g.Hs); break;
+    case 2: sd_kernel<2><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws, g.Hs); break;
+    default: sd_kernel<3><<<grid, 256, p.sd_smem, s>>>(Lorg, Rorg, Ls, Rs, g.W, g.H, g.Ws, g.Hs); break;
   }
   return cudaGetLastError();
 }
@@ -142,8 +136,9 @@ struct PrepArgs {
   uint16_t* pix1;
   uint32_t* arm0;
   uint32_t* arm1;
-  uint32_t* xrow;  // [4][Hs][Wp]: x-pass code L, R; window offsets L, R
+  uint32_t* xrow;  // [4][NB*Hs][Wp]: x-pass code L, R; window offsets L, R
   int Ws, Hs, Wp, w_x, w_x_r, w_y, delta;  // w_x: left image (D^L) x cap, w_x_r: right
+  int plane_rows;  // NB*Hs: rows of one xrow plane (frame f at rows f*Hs ..)
   int P4, BW, Q4, AV;  // strip pads and pitches in bytes (prep_geometry)
   int8_t cdx[6], cdy[6];
 };
@@ -267,7 +262,10 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   uint8_t* sV = sB + (TH + 4) * BW;                   // [32][AV]  vertical strip, column-major
   uint8_t* sYM = sV + 32 * AV;                        // [TH][32]  M (up) of the tile pixels
   uint8_t* sYN = sYM + TH * 32;                       // [TH][32]  N (down)
-  const uint8_t* img = blockIdx.z ? a.img1 : a.img0;
+  // blockIdx.z = 2 * frame + image (0: left, 1: right)
+  const int im = blockIdx.z & 1, fr = blockIdx.z >> 1;
+  const size_t foff = (size_t)fr * Ws * Hs;
+  const uint8_t* img = (im ? a.img1 : a.img0) + foff;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TH;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   constexpr int NW = TH / 4;  // warps
@@ -320,7 +318,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   __syncthreads();
 
   const uint32_t dl4 = (uint32_t)(a.delta >= 128 ? a.delta - 128 : a.delta) * 0x01010101u;
-  const int wx = blockIdx.z ? a.w_x_r : a.w_x;  // per-base x cap
+  const int wx = im ? a.w_x_r : a.w_x;  // per-base x cap
 
   // ---- y arms: thread (column x0 + lane, rows y0 + 4 warp .. +3)
   {
@@ -364,8 +362,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   if (y >= Hs) return;
   const uint32_t M4 = *reinterpret_cast<const uint32_t*>(sYM + r * 32 + 4 * g);
   const uint32_t N4 = *reinterpret_cast<const uint32_t*>(sYN + r * 32 + 4 * g);
-  const size_t plane = (size_t)Hs * a.Wp;
-  uint32_t* xr = a.xrow + blockIdx.z * plane + (size_t)y * a.Wp + xb;  // 16-B aligned (Wp = 32C)
+  const size_t plane = (size_t)a.plane_rows * a.Wp;
+  uint32_t* xr = a.xrow + im * plane + ((size_t)fr * Hs + y) * a.Wp + xb;  // 16-B aligned (Wp = 32C)
   const uint32_t mnl = __byte_perm(m4, n4, 0x5140), mnh = __byte_perm(m4, n4, 0x7362);
   const uint32_t MNl = __byte_perm(M4, N4, 0x5140), MNh = __byte_perm(M4, N4, 0x7362);
   const uint32_t armw[4] = {__byte_perm(mnl, MNl, 0x5410), __byte_perm(mnl, MNl, 0x7632),
@@ -380,8 +378,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     offw[i] = 4u * (x - m) | (4u * (x + n + 1)) << 16;
   }
   if (xb + 3 < Ws) {
-    uint16_t* pix = (blockIdx.z ? a.pix1 : a.pix0) + (size_t)y * Ws + xb;
-    uint32_t* arm = (blockIdx.z ? a.arm1 : a.arm0) + (size_t)y * Ws + xb;
+    uint16_t* pix = (im ? a.pix1 : a.pix0) + foff + (size_t)y * Ws + xb;
+    uint32_t* arm = (im ? a.arm1 : a.arm0) + foff + (size_t)y * Ws + xb;
     *reinterpret_cast<uint4*>(xr) = make_uint4(codew[0], codew[1], codew[2], codew[3]);
     *reinterpret_cast<uint4*>(xr + 2 * plane) = make_uint4(offw[0], offw[1], offw[2], offw[3]);
 #pragma unroll
@@ -400,8 +398,8 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
       if (x < Ws) {
         xr[i] = codew[i];
         xr[2 * plane + i] = offw[i];
-        (blockIdx.z ? a.arm1 : a.arm0)[(size_t)y * Ws + x] = armw[i];
-        (blockIdx.z ? a.pix1 : a.pix0)[(size_t)y * Ws + x] = (uint16_t)(pixw[i >> 1] >> (16 * (i & 1)));
+        (im ? a.arm1 : a.arm0)[foff + (size_t)y * Ws + x] = armw[i];
+        (im ? a.pix1 : a.pix0)[foff + (size_t)y * Ws + x] = (uint16_t)(pixw[i >> 1] >> (16 * (i & 1)));
       } else if (x < a.Wp) {  // pitch padding of the x-pass rows: harmless windows, never read
         xr[i] = 0u;
         xr[2 * plane + i] = 4u * x | (4u * (x + 1)) << 16;
@@ -412,7 +410,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
 
 static int prep_rows_for(const Geom& g, int nsm) {
   for (int pr : {4, 2})
-    if ((long long)(g.Wp / 32) * ((g.Hs + 8 * pr - 1) / (8 * pr)) * 2 >= 4LL * nsm) return pr;
+    if ((long long)(g.Wp / 32) * ((g.Hs + 8 * pr - 1) / (8 * pr)) * 2 * g.NB >= 4LL * nsm) return pr;
   return 1;
 }
 
@@ -435,7 +433,7 @@ static void prep_geometry(const Geom& g, int th, int& P4, int& BW, int& Q4, int&
 static int prep_smem_bytes(int th, int BW, int AV) { return (th + 4) * BW + 32 * AV + 2 * th * 32 + 16; }
 
 cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs,
-                        bool padded, Buffers& b, cudaStream_t s) {
+                        bool padded, Buffers& b, int nfr, cudaStream_t s) {
   PrepArgs a;
   a.img0 = Ls; a.img1 = Rs;
   a.pix0 = b.pixL; a.pix1 = b.pixR;
@@ -443,10 +441,11 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
   a.xrow = b.xrow;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Wp = g.Wp; a.w_x = g.w_x; a.w_x_r = g.w_x_r; a.w_y = g.w_y;
   a.delta = g.delta;
+  a.plane_rows = g.NB * g.Hs;
   const int th = 8 * p.prep_rows;
   prep_geometry(g, th, a.P4, a.BW, a.Q4, a.AV);
   for (int i = 0; i < 6; ++i) { a.cdx[i] = g.cdx[i]; a.cdy[i] = g.cdy[i]; }
-  dim3 grid(g.Wp / 32, (g.Hs + th - 1) / th, 2);
+  dim3 grid(g.Wp / 32, (g.Hs + th - 1) / th, 2 * nfr);
   const int smem = p.prep_smem;
   if (th == 32) {
     if (padded) prep_kernel<32, true><<<grid, 256, smem, s>>>(a);
@@ -459,393 +458,6 @@ cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const u
     else prep_kernel<8, false><<<grid, 64, smem, s>>>(a);
   }
   return cudaGetLastError();
-}
-
-// ============================================================================
-// XPASS — cost (Eqs. 3-5) + x aggregation (Eq. 7) for
-// BOTH bases, Step3.  The right base reuses the left cost line
-// (Eq. 6): C^R(x,d) = C^L(x+d,d), so ONE exclusive prefix row
-//   P[k] = sum_{x'<k} Q(x',d)   (u32, modular: window sums < 2^32 are exact)
-// gives  CA^L_x(x,d) = P[x+n_L+1] - P[x-m_L]
-//        CA^R_x(x,d) = P[x+d+n_R+1] - P[x+d-m_R]
-// with P extended by BORDER = 2^(f+1) per column beyond Ws, replacing
-// the paper's O(W_x) direct sums by O(1) differences.
-// Persistent: one CTA per SM owns a contiguous range of work items
-// (row y, disparity group of ND); every warp takes items independently.  The
-// four PREP row arrays of a row (codes, window offsets; pitch Wp) arrive by
-// bulk asynchronous copies into a ring of `slots` row slots, completed on an
-// mbarrier; the warp that finishes the last item of a row in the range
-// refills its slot with the row `slots` ahead, so row loads overlap compute
-// and no CTA-wide barrier is needed after the start.  Per item:
-//   phase A: lane l scans its contiguous chunk [lC, lC+C) (C odd -> shared
-//            loads at stride C are bank-conflict free); costs from the fixed
-//            tables Q_AD[|dI|] and Q_MC[cL ^ cR] (popc folded into a 64-entry
-//            table), both replicated per bank (index*32 + lane); branch-free
-//            BORDER select for x < d;
-//   warp scan of the 32 lane totals (shuffles) -> P into shared memory;
-//   phase C: lanes interleaved over x -> two coalesced 128-B stores per warp
-//            and disparity.
-// ND = 2: two consecutive disparities d, d+1 per item.  The right pixel of
-// (x, d+1) is the one of (x-1, d), so both cost rows come from the same C + 1
-// shared loads per lane, both window sets from the same offsets, and the two
-// shuffle scans overlap.
-// Output layout: u32 [ceil(Ds/2)][Hs][Wp][2] (disparity pairs interleaved; Wp = 32C).
-// ============================================================================
-struct XArgs {
-  const uint32_t* xrow;  // [4][Hs][Wp]
-  const uint32_t* qad;
-  const uint32_t* qmc;
-  uint32_t* caxL;
-  uint32_t* caxR;
-  int Ws, Hs, Ds, Wp, PL, ext;
-  uint32_t border;
-  int slots;  // row slots in the ring (2..kXMaxSlots)
-  uint32_t mc_mask;  // 63, as a parameter (see the Q_MC address below)
-  const uint32_t* qtab;  // the replicated tables as laid out in shared memory (40 KB)
-};
-
-constexpr int kXMaxWarps = 16;
-constexpr int kXMaxSlots = 4;
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void xbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void xbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "XWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra XWAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// one row's four arrays into a slot (single thread)
-__device__ __forceinline__ void xpass_load_row(uint32_t* slot, uint64_t* bar, const XArgs& a,
-                                               int row) {
-  const uint32_t bytes = (uint32_t)a.Wp * 4u;
-  const size_t plane = (size_t)a.Hs * a.Wp;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(4u * bytes)
-               : "memory");
-  for (int k = 0; k < 4; ++k)
-    bulk_g2s(slot + k * a.Wp, a.xrow + k * plane + (size_t)row * a.Wp, bytes, bar);
-}
-
-// Phase C of an item: CA_x of the lane's columns x = lane + 32 i for both
-// bases from the exclusive prefix rows (L: P_d, P_{d+1}; R: the same rows
-// shifted by d, resp. d + 1); the pair (d, d+1) of a pixel is one 8-B store
-// (CA_x layout u32 [Ds/2][Hs][Wp][2]), 256 coalesced bytes per warp.
-// MODE 2: disparities d and d+1 (one 8-B store per pixel); 1: d only, the
-// d+1 slot zero (odd-Ds tail of the two-disparity kernel); 0: d only, a 4-B
-// store into slot d & 1 (the one-disparity kernel for very wide images).
-template <int C, int MODE>
-__device__ __forceinline__ void xpass_windows(const uint32_t* sAL, const uint32_t* sAR,
-                                              const char* P0, const char* P0d, const char* P1,
-                                              const char* P1d, uint2* outL, uint2* outR, int lane,
-                                              int slot) {
-#pragma unroll
-  for (int i = 0; i < C; ++i) {
-    const uint32_t al = sAL[lane + 32 * i], ar = sAR[lane + 32 * i];
-    const uint32_t alo = al & 0xffffu, ahi = al >> 16, arlo = ar & 0xffffu, arhi = ar >> 16;
-    const uint32_t caL = *reinterpret_cast<const uint32_t*>(P0 + ahi) -
-                         *reinterpret_cast<const uint32_t*>(P0 + alo);
-    const uint32_t caR = *reinterpret_cast<const uint32_t*>(P0d + arhi) -
-                         *reinterpret_cast<const uint32_t*>(P0d + arlo);
-    // pitch Wp = 32C: padding columns are written, never read
-    if (MODE == 0) {
-      reinterpret_cast<uint32_t*>(outL + 32 * i)[slot] = caL;
-      reinterpret_cast<uint32_t*>(outR + 32 * i)[slot] = caR;
-    } else {
-      uint32_t caL1 = 0u, caR1 = 0u;
-      if (MODE == 2) {
-        caL1 = *reinterpret_cast<const uint32_t*>(P1 + ahi) - *reinterpret_cast<const uint32_t*>(P1 + alo);
-        caR1 = *reinterpret_cast<const uint32_t*>(P1d + arhi) - *reinterpret_cast<const uint32_t*>(P1d + arlo);
-      }
-      outL[32 * i] = make_uint2(caL, caL1);
-      outR[32 * i] = make_uint2(caR, caR1);
-    }
-  }
-}
-
-// FIXPL: the per-disparity prefix rows have the compile-time pitch 32C + 128
-// (usable when D_s + w_x + 3 <= 128), so that P_{d+1} = P_d + constant folds
-// into the shared-load immediates instead of one add per window read.
-constexpr int kXFixExt = 128;
-constexpr int kXMaxC2 = 27;  // widest lane chunk kept in registers in one pass
-template <int C, int ND, bool FIXPL>
-__global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
-  static_assert(ND == 1 || ND == 2, "one or two disparities per item");
-  const int PL = FIXPL ? 32 * C + kXFixExt : a.PL;
-  extern __shared__ __align__(128) uint32_t xsm[];
-  uint32_t* sQAD = xsm;                // [256][32]  Q_AD[|dI|], one copy per bank
-  uint32_t* sQMC = sQAD + 256 * 32;    // [64][32]   Q_MC[popc(cL ^ cR)], indexed by cL ^ cR
-  uint32_t* ring = sQMC + 64 * 32;     // [slots][4][32C] row slots
-  const int nw = blockDim.x >> 5;
-  const int nslot = a.slots;
-  uint32_t* Pall = ring + nslot * 4 * 32 * C;  // [nw][ND][PL] exclusive prefixes (+ BORDER)
-  uint64_t* full = reinterpret_cast<uint64_t*>(Pall + (size_t)nw * ND * PL);  // [slots]
-  uint64_t* empty = full + kXMaxSlots;                                          // [slots]
-  uint64_t* tabbar = empty + kXMaxSlots;                                        // [1]
-  unsigned* done = reinterpret_cast<unsigned*>(tabbar + 1);                     // [slots]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* P = Pall + warp * ND * PL;
-
-  // this CTA's item range [i0, i1) of the Hs * npairs items, and its rows
-  const int npairs = (a.Ds + ND - 1) / ND;
-  const long long total = (long long)a.Hs * npairs;
-  const int i0 = (int)(total * blockIdx.x / gridDim.x);
-  const int i1 = (int)(total * (blockIdx.x + 1) / gridDim.x);
-  if (i0 >= i1) return;
-  const int rfirst = i0 / npairs, rlast = (i1 - 1) / npairs;
-  const int skip0 = i0 - rfirst * npairs;  // items of the first row owned by earlier CTAs
-
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < nslot; ++k) {
-      xbar_init(full + k);
-      // one arrival per item of the slot's row: orders every warp's reads of
-      // the slot before its refill (the counter below only elects the refiller)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + k)), "r"(npairs)
-                   : "memory");
-      done[k] = 0u;
-    }
-    if (skip0)  // items of the first row owned by earlier CTAs
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(empty)),
-                   "r"(skip0)
-                   : "memory");
-    xbar_init(tabbar);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the bank-replicated tables arrive pre-built (one 40 KB bulk copy)
-    constexpr uint32_t kTabBytes = (256 + 64) * 32 * 4;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tabbar)),
-                 "r"(kTabBytes)
-                 : "memory");
-    bulk_g2s(sQAD, a.qtab, kTabBytes, tabbar);
-    for (int k = 0; k < nslot && rfirst + k <= rlast; ++k)
-      xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
-  }
-  __syncthreads();  // barrier inits visible
-  xbar_wait(tabbar, 0u);
-  // with pixels encoded as census | I << 24, |dI|*128 = vabsdiffu4(pl, pr) >> 17 and
-  // (cL ^ cR)*128 = ((pl ^ pr) & 63) << 7: table addresses in two ALU operations.
-  const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
-  const char* qmcb = reinterpret_cast<const char*>(sQMC + lane);
-  // the census mask arrives as a kernel parameter so that it sits in a
-  // register: (pl ^ pr) & mask is then one 3-input LOP3 and the table address
-  // one LEA (a literal 63 lets the compiler shift first and mask 0x1f80 after)
-  const uint32_t mcm = a.mc_mask;
-  const char* Pb = reinterpret_cast<const char*>(P);
-  const int PLb = 4 * PL;
-  const int Ws = a.Ws;
-  const uint32_t border = a.border;
-
-  // item -> (row y, pair p), row -> (ring slot, lap): one division at the
-  // start, then incremental updates (a warp's items are nw apart, nw < npairs
-  // is not assumed: the row advance is a short loop)
-  int y = (i0 + warp) / npairs, pidx = i0 + warp - y * npairs;
-  int slot = (y - rfirst) % nslot, lap = (y - rfirst) / nslot;
-#pragma unroll 1
-  for (int it = i0 + warp; it < i1; it += nw) {
-    const int d = pidx * ND;
-    xbar_wait(full + slot, (uint32_t)lap & 1u);
-    const uint32_t* sL = ring + slot * 4 * 32 * C;
-    const uint32_t* sR = sL + 32 * C;
-    const uint32_t* sAL = sR + 32 * C;
-    const uint32_t* sAR = sAL + 32 * C;
-    const bool two = ND == 2 && d + 1 < a.Ds;
-    // ---- phase A: costs of the lane's chunk + local inclusive prefixes
-    const uint32_t* Lr = sL + lane * C;
-    // elements k < nb have x - d < 0 and take BORDER; their loads land before
-    // sR (in the slot's sL or the tables: d <= 255) and are unused
-    const int nb = d - lane * C;
-    const uint32_t* Rr = sR + lane * C - d;
-    // Register passes of CH columns: one pass when the 2C prefix registers fit
-    // (C <= kXMaxC2), else two (wide rows, C <= 2 kXMaxC2): the first pass's
-    // local prefixes go to shared memory right away and get the lane offset
-    // added after the warp scan (one read-modify-write per element).
-    constexpr int CH = C <= kXMaxC2 ? C : (C + 1) / 2;
-    uint32_t pref[ND][CH];
-    uint32_t run[ND] = {};
-    uint32_t prv = ND == 2 ? Rr[-1] : 0u;  // right pixel of (x, d+1) = of (x-1, d)
-    auto costs = [&](int k0, int kn) {
-#pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        if (j < kn) {
-          const int k = k0 + j;
-          const uint32_t pl = Lr[k], pr = Rr[k];
-          const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
-          const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & mcm) << 7));
-          run[0] += (k < nb) ? border : qa + qm;  // reading R12b: out of the right image
-          pref[0][j] = run[0];
-          if (ND == 2) {
-            const uint32_t qa1 = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, prv) >> 17));
-            const uint32_t qm1 = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ prv) & mcm) << 7));
-            run[ND - 1] += (k < nb + 1) ? border : qa1 + qm1;
-            pref[ND - 1][j] = run[ND - 1];
-            prv = pr;
-          }
-        }
-      }
-    };
-    if (CH < C) {  // first pass, stored without the lane offset
-      costs(0, CH);
-#pragma unroll
-      for (int n = 0; n < ND; ++n) {
-        uint32_t* Pl = P + n * PL + lane * C + 1;
-#pragma unroll
-        for (int j = 0; j < CH; ++j) Pl[j] = pref[n][j];
-      }
-    }
-    costs(C - CH == 0 ? 0 : CH, C - (CH < C ? CH : 0));
-    uint32_t incl[ND];
-#pragma unroll
-    for (int n = 0; n < ND; ++n) incl[n] = run[n];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-      for (int n = 0; n < ND; ++n) {
-        const uint32_t t = __shfl_up_sync(kFull, incl[n], o);
-        if (lane >= o) incl[n] += t;
-      }
-    }
-#pragma unroll
-    for (int n = 0; n < ND; ++n) {
-      const uint32_t off = incl[n] - run[n];
-      uint32_t* Pl = P + n * PL + lane * C + 1;
-      if (CH < C) {
-#pragma unroll
-        for (int j = 0; j < CH; ++j) Pl[j] += off;  // first pass: add the offset
-#pragma unroll
-        for (int j = 0; j < C - CH; ++j) Pl[CH + j] = pref[n][j] + off;
-      } else {
-#pragma unroll
-        for (int k = 0; k < C; ++k) Pl[k] = pref[n][k] + off;
-      }
-    }
-    if (lane < ND) P[lane * PL] = 0;
-    __syncwarp();
-    uint32_t PW[ND];
-#pragma unroll
-    for (int n = 0; n < ND; ++n) PW[n] = P[n * PL + Ws];
-    for (int e = lane; e < a.ext; e += 32) {
-#pragma unroll
-      for (int n = 0; n < ND; ++n) P[n * PL + Ws + 1 + e] = PW[n] + (uint32_t)(e + 1) * border;
-    }
-    __syncwarp();
-    // ---- phase C: window differences (precomputed byte offsets), coalesced stores
-    uint2* outL = reinterpret_cast<uint2*>(a.caxL) + ((size_t)(d >> 1) * a.Hs + y) * a.Wp + lane;
-    uint2* outR = reinterpret_cast<uint2*>(a.caxR) + ((size_t)(d >> 1) * a.Hs + y) * a.Wp + lane;
-    const char* Pdb = Pb + 4 * d;
-    if (ND == 1)
-      xpass_windows<C, 0>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, lane, d & 1);
-    else if (two)  // (the single-disparity tail item exists only for odd Ds)
-      xpass_windows<C, 2>(sAL, sAR, Pb, Pdb, Pb + PLb, Pdb + PLb + 4, outL, outR, lane, 0);
-    else
-      xpass_windows<C, 1>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, lane, 0);
-    __syncwarp();
-    // ---- release the row slot: the warp finishing the row's last item of
-    // this range refills the slot with the row `slots` ahead
-    if (lane == 0) {
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot))
-                   : "memory");
-      const unsigned target = (unsigned)((lap + 1) * npairs - (slot == 0 ? skip0 : 0));
-      const unsigned prev = atomicAdd(done + slot, 1u);
-      if (prev + 1u == target && y + nslot <= rlast) {
-        xbar_wait(empty + slot, (uint32_t)lap & 1u);  // complete: this was the last item
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        xpass_load_row(ring + slot * 4 * 32 * C, full + slot, a, y + nslot);
-      }
-    }
-    for (pidx += nw; pidx >= npairs; pidx -= npairs) {  // next item of this warp
-      ++y;
-      if (++slot == nslot) { slot = 0; ++lap; }
-    }
-  }
-}
-
-int xpass_chunk_for(int Ws) {
-  for (int c = 3; c <= 63; c += 2)
-    if (32 * c >= Ws) return c;
-  return 0;
-}
-
-// two disparities per item while the prefix registers of one or two register
-// passes (2 * ceil(C/2)) fit
-template <int C>
-constexpr int xpass_nd() { return C <= 2 * kXMaxC2 ? 2 : 1; }
-
-template <int C>
-static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
-  XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, g.border, p.xpass_slots, 63u, b.qtab};
-  if (p.xpass_fixpl)
-    xpass_kernel<C, xpass_nd<C>(), true><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
-  else
-    xpass_kernel<C, xpass_nd<C>(), false><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename F>
-static cudaError_t max_carveout(F fn);
-
-template <int C>
-static cudaError_t setup_xpass_c(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = max_carveout(xpass_kernel<C, xpass_nd<C>(), true>);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(xpass_kernel<C, xpass_nd<C>(), false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = max_carveout(xpass_kernel<C, xpass_nd<C>(), false>);
-  return e;
-}
-
-#define XPASS_DISPATCH(C_, EXPR)                        \
-  switch (C_) {                                         \
-    case 3: { constexpr int CC = 3; EXPR; } break;   \
-    case 5: { constexpr int CC = 5; EXPR; } break;   \
-    case 7: { constexpr int CC = 7; EXPR; } break;   \
-    case 9: { constexpr int CC = 9; EXPR; } break;   \
-    case 11: { constexpr int CC = 11; EXPR; } break;   \
-    case 13: { constexpr int CC = 13; EXPR; } break;   \
-    case 15: { constexpr int CC = 15; EXPR; } break;   \
-    case 17: { constexpr int CC = 17; EXPR; } break;   \
-    case 19: { constexpr int CC = 19; EXPR; } break;   \
-    case 21: { constexpr int CC = 21; EXPR; } break;   \
-    case 23: { constexpr int CC = 23; EXPR; } break;   \
-    case 25: { constexpr int CC = 25; EXPR; } break;   \
-    case 27: { constexpr int CC = 27; EXPR; } break;   \
-    case 29: { constexpr int CC = 29; EXPR; } break;   \
-    case 31: { constexpr int CC = 31; EXPR; } break;   \
-    case 33: { constexpr int CC = 33; EXPR; } break;   \
-    case 35: { constexpr int CC = 35; EXPR; } break;   \
-    case 37: { constexpr int CC = 37; EXPR; } break;   \
-    case 39: { constexpr int CC = 39; EXPR; } break;   \
-    case 41: { constexpr int CC = 41; EXPR; } break;   \
-    case 43: { constexpr int CC = 43; EXPR; } break;   \
-    case 45: { constexpr int CC = 45; EXPR; } break;   \
-    case 47: { constexpr int CC = 47; EXPR; } break;   \
-    case 49: { constexpr int CC = 49; EXPR; } break;   \
-    case 51: { constexpr int CC = 51; EXPR; } break;   \
-    case 53: { constexpr int CC = 53; EXPR; } break;   \
-    case 55: { constexpr int CC = 55; EXPR; } break;   \
-    case 57: { constexpr int CC = 57; EXPR; } break;   \
-    case 59: { constexpr int CC = 59; EXPR; } break;   \
-    case 61: { constexpr int CC = 61; EXPR; } break;   \
-    case 63: { constexpr int CC = 63; EXPR; } break;   \
-    default: break;                                     \
-  }
-
-cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
-  cudaError_t e = cudaErrorInvalidValue;
-  XPASS_DISPATCH(p.xpass_C, e = launch_xpass_c<CC>(g, p, b, s));
-  return e;
 }
 
 // ============================================================================
@@ -873,6 +485,7 @@ struct YArgs {
   uint64_t* ca0;  // debug (may be null)
   uint64_t* ca1;
   int Ws, Hs, Ds, w_y, B;
+  int y_begin, y_end;  // output rows of this launch (tiles of B rows from y_begin)
   uint32_t e52;  // kYExp52
 };
 
@@ -1024,11 +637,11 @@ __global__ void __launch_bounds__(kYThreads, 2)
   uint8_t* dmap = base ? a.D1 : a.D0;
   uint64_t* cadbg = base ? a.ca1 : a.ca0;
   const int x0 = blockIdx.x * 16, x = x0 + col;
-  const int y0 = blockIdx.y * a.B, yt0 = y0 - a.w_y;
+  const int y0 = a.y_begin + blockIdx.y * a.B, yt0 = y0 - a.w_y;
   const int Ds = a.Ds;
   // output rows of this thread: y0 + seg + 16 r, r < nr (interleaved, so the
   // rows past B are whole trailing iterations, mostly warp-uniform)
-  const int nrow = min(a.B, a.Hs - y0);
+  const int nrow = min(a.B, a.y_end - y0);
   const int nr = max(0, (nrow - seg + 15) >> 4);  // same for both segments of a warp if B even
   // (B odd: the two half-warps may differ by one row; the warp then runs the
   // larger count and the extra row reads a harmless window, never stored)
@@ -1151,7 +764,7 @@ static int ypass_smem_bytes(int SEG) {
 
 
 
-cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
+cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca, int nfr,
                          cudaStream_t s) {
   YArgs a;
   a.arm0 = b.armL; a.arm1 = b.armR;
@@ -1159,8 +772,12 @@ cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
+  // whole frames (the batch as one image of nfr*Hs rows), or in band mode
+  // only the rows whose D^L / D^R the band's POST reads
+  a.y_begin = g.band ? g.ya : 0;
+  a.y_end = g.band ? g.yb : nfr * g.Hs;
   a.e52 = kYExp52;
-  dim3 grid((g.Ws + 15) / 16, p.ypass_nb, 2);
+  dim3 grid((g.Ws + 15) / 16, (a.y_end - a.y_begin + p.ypass_B - 1) / p.ypass_B, 2);
   cudaError_t e = cudaErrorInvalidValue;
   if (store_ca)
     YPASS_DISPATCH(p.ypass_SEG,
@@ -1203,14 +820,29 @@ struct PostArgs {
   uint8_t* median;
   float* fill;
   float* out;
-  int32_t* rowFirst;
-  int32_t* rowLast;
+  int32_t* rowFirst;  // [4][Hs] of this frame: first x, last x, first value, last value
+  int32_t* rowLast;   // = rowFirst + Hs
   unsigned* counter;
   int W, H, Ws, Hs, K, T;
   int fill_mode;  // STEREO_FILL_*
   int Wsp;  // smem row pitch, post_pitch(Ws)
   int Wx;   // W rounded up to 4
+  int y_lo, y_hi;  // scaled rows owned by this launch (band mode: the band's own rows)
+  int out_row0;    // original row held by out[0] (band mode: the first own row)
+  int rule_d;      // resolve fill rule (d) in-kernel (whole frames; band mode: stereo_band_finish)
 };
+
+// the frame `fr` of a batch launch: every per-frame buffer offset by its slot
+__device__ __forceinline__ PostArgs post_frame(PostArgs a, int fr) {
+  const size_t n = (size_t)a.Ws * a.Hs, N = (size_t)a.W * a.H;
+  a.DL += fr * n; a.DR += fr * n; a.pixL += fr * n;
+  a.masked += fr * n; a.median += fr * n; a.fill += fr * n;
+  a.Lorg += fr * N; a.out += fr * N;
+  a.rowFirst += (size_t)fr * 4 * a.Hs;
+  a.rowLast = a.rowFirst + a.Hs;
+  a.counter += fr;
+  return a;
+}
 
 // u16x2 helpers of the SIMD median (lanes hold values 0..255, INVALID = 255)
 __device__ __forceinline__ void cswap16(uint32_t& a, uint32_t& b) {
@@ -1305,7 +937,7 @@ __device__ void su_row_global(const PostArgs& a, int Y, float thr) {
       v = __fmul_rn(__fadd_rn(v, su_xval(a.fill + (size_t)yb * a.Ws,
                                          a.Lorg + (size_t)(2 * yb) * a.W, X, a.W, a.Ws, thr)),
                     0.5f);
-    a.out[(size_t)Y * a.W + X] = v;
+    a.out[(size_t)(Y - a.out_row0) * a.W + X] = v;
   }
 }
 
@@ -1327,7 +959,8 @@ __device__ __forceinline__ void stage_row(uint8_t* dst, const uint8_t* src, int 
 }
 
 template <int R>  // scaled rows owned per CTA
-__global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
+__global__ void __launch_bounds__(512) post_kernel(PostArgs a0) {
+  const PostArgs a = post_frame(a0, blockIdx.z);
   extern __shared__ uint32_t psm_[];
   const int Ws = a.Ws, Wsp = a.Wsp, nch = Wsp >> 5, W = a.W, Wx = a.Wx;
   uint8_t* mk = reinterpret_cast<uint8_t*>(psm_);                  // [R+3][Wsp] masked rows
@@ -1343,8 +976,8 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   uint8_t* sLo = sDR + (R + 3) * Wsp;                                      // [R+1][Wx] L_org rows
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int y0 = blockIdx.x * R;
-  const int nr = min(R, a.Hs - y0);                          // owned scaled rows
+  const int y0 = a.y_lo + blockIdx.x * R;
+  const int nr = min(R, a.y_hi - y0);                        // owned scaled rows
   const int nf = a.K == 2 ? min(nr + 1, a.Hs - y0) : nr;     // fill rows needed (SU reads y+1)
   const float thr = (float)(a.K * a.T);
 
@@ -1518,7 +1151,10 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
         v = fill_value(mdr, pix, x, li, ri, a.T, a.fill_mode);
       }
       fv[j * Wsp + x] = v;
-      if (j < nr) (a.K == 2 ? a.fill : a.out)[(size_t)(y0 + j) * Ws + x] = v;
+      if (j < nr) {
+        if (a.K == 2) a.fill[(size_t)(y0 + j) * Ws + x] = v;
+        else a.out[(size_t)(y0 + j - a.out_row0) * Ws + x] = v;
+      }
     }
   }
   if (a.K == 2) {
@@ -1557,7 +1193,7 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
       const float* x0r = xr + j * Wx;
       const float* x1r = xr + (j + 1) * Wx;
       const bool down = j + 1 < nf;
-      float* o0 = a.out + (size_t)(2 * y) * W;
+      float* o0 = a.out + (size_t)(2 * y - a.out_row0) * W;
       float* o1 = o0 + W;
       const bool has1 = 2 * y + 1 < a.H;
       const bool extra = (y == a.Hs - 1) && (2 * y + 2 < a.H);
@@ -1573,6 +1209,7 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
     }
   }
   // 7. rule (d): the last CTA patches rows with no valid pixel
+  if (!a.rule_d) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
@@ -1604,51 +1241,102 @@ __global__ void __launch_bounds__(512) post_kernel(PostArgs a) {
   if (tid == 0) *a.counter = 0u;
 }
 
-// Rule (d) patch for band mode: rows whose value only global information fixes
-// (dist.py exchanges the per-row summaries).  One CTA: set the rows, then redo
-// Step8 for the output rows that read them.
-__global__ void __launch_bounds__(256) patch_kernel(PostArgs a, const int32_t* rows,
-                                                    const float* vals, int n) {
-  for (int i = 0; i < n; ++i) {
-    float* dst = (a.K == 2 ? a.fill : a.out) + (size_t)rows[i] * a.Ws;
-    for (int x = threadIdx.x; x < a.Ws; x += blockDim.x) dst[x] = vals[i];
+// Band mode: the frame-wide per-row summary that fill rule (d)
+// needs (R25b: an all-invalid row takes the last valid value of the nearest
+// row above that has one, else the first valid value of the nearest row
+// below, else 0).  summ: int32 [Hs_g][2] = (last valid value, first valid
+// value), -1 = none; this band writes its own rows and -1 everywhere else, so
+// an element-wise MAX over the bands (one NCCL all_reduce) assembles the frame.
+__global__ void __launch_bounds__(256) band_summary_kernel(const int32_t* __restrict__ rowFirst,
+                                                           int32_t* __restrict__ summ, int Hs,
+                                                           int s0, int Hs_g, int pa, int pb) {
+  for (int yg = blockIdx.x * blockDim.x + threadIdx.x; yg < Hs_g; yg += gridDim.x * blockDim.x) {
+    const int y = yg - s0;
+    int2 v = make_int2(-1, -1);
+    if (y >= pa && y < pb) v = make_int2(rowFirst[3 * Hs + y], rowFirst[2 * Hs + y]);
+    reinterpret_cast<int2*>(summ)[yg] = v;
   }
-  __syncthreads();
-  if (a.K != 2) return;
-  const float thr = (float)(a.K * a.T);
-  for (int i = 0; i < n; ++i)
-    for (int Y = max(2 * rows[i] - 1, 0); Y <= min(2 * rows[i] + 2, a.H - 1); ++Y) su_row_global(a, Y, thr);
 }
 
-cudaError_t launch_patch(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out,
-                         const int32_t* rows_dev, const float* vals_dev, int n, cudaStream_t s) {
-  PostArgs a;
-  a.DL = b.DL; a.DR = b.DR; a.pixL = b.pixL; a.Lorg = Lorg;
-  a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
-  a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
-  a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
-  a.fill_mode = g.fill_mode;
-  a.Wsp = post_pitch(g.Ws);
-  a.Wx = (g.W + 3) & ~3;
-  patch_kernel<<<1, 256, 0, s>>>(a, rows_dev, vals_dev, n);
+// Rule (d) for the rows this band's output reads (own rows and, K = 2, the
+// next band's first row, which Step8's odd rows read), from the frame-wide
+// summaries; then Step8 again for the own output rows that read a patched
+// fill row.  One CTA; returns at once when no such row is all-invalid.
+__global__ void __launch_bounds__(256) band_finish_kernel(PostArgs a, const int32_t* __restrict__ summ,
+                                                          int s0, int Hs_g, int out_rows) {
+  const int pa = a.y_lo, pb = a.y_hi;
+  const int hi = min(pb + (a.K == 2 ? 1 : 0), Hs_g - s0);
+  int mine = 0;
+  for (int y = pa + threadIdx.x; y < hi; y += blockDim.x) mine |= summ[2 * (y + s0)] < 0;
+  if (!__syncthreads_or(mine)) return;
+  for (int y = pa; y < hi; ++y) {
+    if (summ[2 * (y + s0)] >= 0) continue;
+    float v = 0.0f;
+    int yy = y + s0 - 1;
+    while (yy >= 0 && summ[2 * yy] < 0) --yy;
+    if (yy >= 0) {
+      v = (float)summ[2 * yy];
+    } else {
+      yy = y + s0 + 1;
+      while (yy < Hs_g && summ[2 * yy + 1] < 0) ++yy;
+      if (yy < Hs_g) v = (float)summ[2 * yy + 1];
+    }
+    if (a.K == 2) {
+      for (int x = threadIdx.x; x < a.Ws; x += blockDim.x) a.fill[(size_t)y * a.Ws + x] = v;
+    } else if (y < pb) {
+      for (int x = threadIdx.x; x < a.Ws; x += blockDim.x) a.out[(size_t)(y - a.out_row0) * a.Ws + x] = v;
+    }
+  }
+  if (a.K != 2) return;
+  __threadfence_block();
+  __syncthreads();
+  const float thr = (float)(a.K * a.T);
+  const int Y0 = a.out_row0, Y1 = a.out_row0 + out_rows;  // own output rows (sub-image coordinates)
+  for (int y = pa; y < hi; ++y) {
+    if (summ[2 * (y + s0)] >= 0) continue;
+    for (int Y = max(2 * y - 1, Y0); Y <= min(2 * y + 2, Y1 - 1); ++Y) su_row_global(a, Y, thr);
+  }
+}
+
+static PostArgs post_args(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out);
+
+cudaError_t launch_band_summary(const Geom& g, Buffers& b, int32_t* summ, cudaStream_t s) {
+  band_summary_kernel<<<(g.Hs_g + 255) / 256, 256, 0, s>>>(b.rowFirst, summ, g.Hs, g.s0, g.Hs_g,
+                                                            g.pa, g.pb);
   return cudaGetLastError();
 }
 
-cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
-                        float* out, cudaStream_t s) {
+cudaError_t launch_band_finish(const Geom& g, Buffers& b, const int32_t* summ,
+                               const uint8_t* Lorg, float* out, cudaStream_t s) {
+  band_finish_kernel<<<1, 256, 0, s>>>(post_args(g, b, Lorg, out), summ, g.s0, g.Hs_g, g.rows_org);
+  return cudaGetLastError();
+}
+
+static PostArgs post_args(const Geom& g, Buffers& b, const uint8_t* Lorg, float* out) {
   PostArgs a;
   a.DL = b.DL; a.DR = b.DR; a.pixL = b.pixL; a.Lorg = Lorg;
   a.masked = b.masked; a.median = b.median; a.fill = b.fill; a.out = out;
-  a.rowFirst = b.rowFirst; a.rowLast = b.rowLast; a.counter = b.counter;
+  a.rowFirst = b.rowFirst; a.rowLast = b.rowFirst + g.Hs; a.counter = b.counter;
   a.W = g.W; a.H = g.H; a.Ws = g.Ws; a.Hs = g.Hs; a.K = g.K; a.T = g.t_fill;
   a.fill_mode = g.fill_mode;
   a.Wsp = post_pitch(g.Ws);
   a.Wx = (g.W + 3) & ~3;
-  const int R = p.post_rows, nt = p.post_threads;
-  if (R == 1) post_kernel<1><<<g.Hs, nt, p.post_smem, s>>>(a);
-  else if (R == 2) post_kernel<2><<<(g.Hs + 1) / 2, nt, p.post_smem, s>>>(a);
-  else if (R == 4) post_kernel<4><<<(g.Hs + 3) / 4, nt, p.post_smem, s>>>(a);
-  else post_kernel<8><<<(g.Hs + 7) / 8, nt, p.post_smem, s>>>(a);
+  a.y_lo = g.band ? g.pa : 0;
+  a.y_hi = g.band ? g.pb : g.Hs;
+  a.out_row0 = g.band ? g.top : 0;
+  a.rule_d = g.band ? 0 : 1;
+  return a;
+}
+
+cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
+                        float* out, int nfr, cudaStream_t s) {
+  const PostArgs a = post_args(g, b, Lorg, out);
+  const int R = p.post_rows, nt = p.post_threads, rows = a.y_hi - a.y_lo;
+  const dim3 grid((rows + R - 1) / R, 1, nfr);
+  if (R == 1) post_kernel<1><<<grid, nt, p.post_smem, s>>>(a);
+  else if (R == 2) post_kernel<2><<<grid, nt, p.post_smem, s>>>(a);
+  else if (R == 4) post_kernel<4><<<grid, nt, p.post_smem, s>>>(a);
+  else post_kernel<8><<<grid, nt, p.post_smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1716,35 +1404,15 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
     if (q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
     fn = reinterpret_cast<EncodeTiledFn>(f);
   }
-  cuuint64_t dims[3] = {(cuuint64_t)g.Wp, (cuuint64_t)g.Hs, (cuuint64_t)((g.Ds + 1) / 2)};
-  cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 8, (cuuint64_t)g.Wp * g.Hs * 8};
+  const cuuint64_t rows = (cuuint64_t)g.NB * g.Hs;  // the batch as one tall image
+  cuuint64_t dims[3] = {(cuuint64_t)g.Wp, rows, (cuuint64_t)((g.Ds + 1) / 2)};
+  cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 8, (cuuint64_t)g.Wp * rows * 8};
   cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-// Development knobs (plan overrides for tuning experiments; unset = the
-// planner's choice).  Out-of-range values are clamped.
-static int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return std::max(lo, std::min(hi, std::atoi(v)));
-}
-
-// Kernels of different frames share SMs (frames in flight on several
-// streams); an SM whose L1/shared carveout was sized for a small-shared-memory
-// kernel cannot take an x-pass or y-pass CTA until it is reconfigured, so
-// every kernel asks for the maximum shared carveout (STEREO_CARVEOUT = percent,
-// -1 = the driver's default; measured identical on B200 today, where the
-// driver already picks the maximum for these kernels: kept as a guarantee).
-template <typename F>
-static cudaError_t max_carveout(F fn) {
-  const int pct = env_int("STEREO_CARVEOUT", 100, -1, 100);
-  if (pct < 0) return cudaSuccess;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
@@ -1780,7 +1448,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   for (auto fn : {prep_kernel<32, true>, prep_kernel<32, false>, prep_kernel<16, true>,
                   prep_kernel<16, false>, prep_kernel<8, true>, prep_kernel<8, false>}) {
     if (p.prep_smem > 48 * 1024 &&
-        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.prep_smem)))
+        (e = raise_smem(fn, p.prep_smem)))
       return e;
     if ((e = max_carveout(fn))) return e;
   }
@@ -1790,28 +1458,31 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     if ((e = max_carveout(fn))) return e;
   if (p.post_smem > 48 * 1024) {
     for (auto fn : {post_kernel<1>, post_kernel<2>, post_kernel<4>, post_kernel<8>})
-      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.post_smem)))
+      if ((e = raise_smem(fn, p.post_smem)))
         return e;
   }
   if (p.sd_smem > 48 * 1024) {
     switch (g.m_pool) {
-      case 0: e = cudaFuncSetAttribute(sd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
-      case 1: e = cudaFuncSetAttribute(sd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
-      case 2: e = cudaFuncSetAttribute(sd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
-      default: e = cudaFuncSetAttribute(sd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sd_smem); break;
+      case 0: e = raise_smem(sd_kernel<0>, p.sd_smem); break;
+      case 1: e = raise_smem(sd_kernel<1>, p.sd_smem); break;
+      case 2: e = raise_smem(sd_kernel<2>, p.sd_smem); break;
+      default: e = raise_smem(sd_kernel<3>, p.sd_smem); break;
     }
     if (e != cudaSuccess) return e;
   }
   // YPASS: choose the number of tiles per strip balancing halo cost and waves
   // (per-CTA shared wavefronts per d ~ 1.25*TB + 1.75*B + tot exchange)
+  // rows of one launch: a whole batch of NB frames (one tall image), or in
+  // band mode the rows whose maps the band's POST reads
+  const int yrows = g.band ? g.yb - g.ya : g.NB * g.Hs;
   const int strips = (g.Ws + 15) / 16;
-  const int nb0 = (g.Hs + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
+  const int nb0 = (yrows + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
   p.ypass_nb = 0;
-  const int nb_force = env_int("STEREO_YPASS_NB", 0, 0, g.Hs);
-  for (int nb = nb0; nb <= g.Hs; ++nb) {
+  const int nb_force = env_int("STEREO_YPASS_NB", 0, 0, yrows);
+  for (int nb = nb0; nb <= yrows; ++nb) {
     if (nb_force && nb != nb_force) continue;
-    const int B = (g.Hs + nb - 1) / nb;
+    const int B = (yrows + nb - 1) / nb;
     const int SEG = ypass_seg_for(B + 2 * g.w_y);
     if (!SEG) continue;
     const int smem = ypass_smem_bytes(SEG);
@@ -1829,13 +1500,9 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   if (e != cudaSuccess) return e;
   YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, true>));
   if (e != cudaSuccess) return e;
-  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS, false>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       p.ypass_smem));
+  YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, false>, p.ypass_smem));
   if (e != cudaSuccess) return e;
-  YPASS_DISPATCH(p.ypass_SEG, e = cudaFuncSetAttribute(ypass_kernel<SS, true>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       p.ypass_smem));
+  YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, true>, p.ypass_smem));
   if (e != cudaSuccess) return e;
   // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
   p.xpass_C = xpass_chunk_for(g.Ws);
@@ -1874,7 +1541,7 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     p.xpass_warps = (int)std::min<size_t>(kXMaxWarps, (cap - fixed) / per_warp);
     p.xpass_warps = std::min(p.xpass_warps, env_int("STEREO_XPASS_WARPS", coresident ? 8 : kXMaxWarps, 1, kXMaxWarps));
     p.xpass_smem = (int)(fixed + per_warp * p.xpass_warps);
-    XPASS_DISPATCH(p.xpass_C, e = setup_xpass_c<CC>(p.xpass_smem));
+    e = setup_xpass(p.xpass_C, p.xpass_smem);
     if (e != cudaSuccess) return e;
     p.xpass_grid = nsm;
   }

@@ -1,8 +1,14 @@
-"""Multi-process (gloo, world_size 2 and 3, CPU) tests of the band-mode host
-logic in paper_2212_00488_b200/dist.py: band geometry, the one-step P2P halo
-exchange, the global rule-(d) patch.  The per-band compute is the CPU oracle
-(test infrastructure) so the test runs anywhere; the assembled bands must equal
-the full-frame oracle bit for bit (DESIGN.md §6 correctness criterion)."""
+"""Multi-process (gloo, world_size 2 and 3, CPU) tests of the band-mode
+plumbing in paper_2212_00488_b200/dist.py: the library's band partition and
+halo rules (host functions of the C ABI, no GPU needed), the one-step P2P halo
+exchange into the preallocated sub-images, and the MAX all-reduce that
+assembles the frame-wide fill summaries.
+
+The per-band compute here is the CPU oracle (test infrastructure), run on the
+exchanged sub-image: its own rows must equal the full-frame oracle bit for bit
+(the halo covers the dependency cone) except where fill rule (d) needs other
+bands' rows, which the test resolves from the all-reduced summaries exactly as
+stereo_band_finish does on the GPU (DESIGN.md §6 correctness criterion)."""
 import os
 import socket
 
@@ -10,6 +16,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_2212_00488_b200 import abi
 from paper_2212_00488_b200 import dist as sdist
 from paper_2212_00488_b200 import synth
 
@@ -22,31 +29,22 @@ def _free_port():
     return p
 
 
-def _oracle_band(Lb, Rb, D, K, w_y, rank, bands, H):
-    """Band compute with the oracle + the same rule-(d) patch dist.py applies."""
-    import torch
-    import torch.distributed as dist
-    p = oracle.params(k_scale=K, w_y=w_y)
-    r = oracle.pipeline(Lb, Rb, D, p, "fixed", stages=("median", "fill", "out"))
-    b = bands[rank]
-    Hs = H // K
-    s0 = b.r0 // K
-    med = r["median"]
+def _summaries(med):
+    """(last valid value, first valid value) per row, -1 = none."""
     valid = med != 255
-    own = slice(b.ys0 - s0, b.ys1 - s0)
-    has = valid[own].any(axis=1).astype(np.int64)
-    first = np.array([row[np.argmax(v)] if v.any() else -1 for row, v in zip(med[own], valid[own])])
-    last = np.array([row[len(v) - 1 - np.argmax(v[::-1])] if v.any() else -1
-                     for row, v in zip(med[own], valid[own])])
-    summ = sdist.gather_row_summaries(np.stack([has, first, last]), b, Hs, dist, "cpu")
-    rows, vals = sdist.rule_d_patches(summ, b, K, med.shape[0])
-    out = r["out"]
-    if len(rows):
-        fill = r["fill"].copy()
-        for y, v in zip(rows, vals):
-            fill[y] = v
-        out = fill if K == 1 else oracle.scale_up(fill, Lb, K, p.t_fill)
-    return out[b.o0 - b.r0:b.o1 - b.r0]
+    last = np.array([row[len(v) - 1 - np.argmax(v[::-1])] if v.any() else -1 for row, v in zip(med, valid)])
+    first = np.array([row[np.argmax(v)] if v.any() else -1 for row, v in zip(med, valid)])
+    return np.stack([last, first], axis=1).astype(np.int32)
+
+
+def _rule_d_value(summ, y):
+    for yy in range(y - 1, -1, -1):
+        if summ[yy, 0] >= 0:
+            return float(summ[yy, 0])
+    for yy in range(y + 1, summ.shape[0]):
+        if summ[yy, 1] >= 0:
+            return float(summ[yy, 1])
+    return 0.0
 
 
 def _worker(rank, world, port, case, q):
@@ -56,38 +54,65 @@ def _worker(rank, world, port, case, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        W, H, D, K, w_y, kind = case
+        W, H, D, K, w_y, m_pool, kind = case
         if kind == "scene":
             L, R, _ = synth.scene(W, H, D, seed=11)
         else:  # unrelated noise: many rows without a single GCP (rule (d))
             L, R = synth.random_pair(W, H, seed=5, levels=256)
-        bands = sdist.band_plan(H, world, K, w_y)
-        b = bands[rank]
-        a0, a1 = sdist.owned_rows(b, H, K)
-        Lown = torch.from_numpy(L[a0:a1].copy())
-        Rown = torch.from_numpy(R[a0:a1].copy())
-        Lb, Rb = sdist.exchange_halos(Lown, Rown, bands, rank, H, K, dist)
-        assert np.array_equal(Lb.numpy(), L[b.r0:b.r1]) and np.array_equal(Rb.numpy(), R[b.r0:b.r1])
-        mine = _oracle_band(Lb.numpy(), Rb.numpy(), D, K, w_y, rank, bands, H)
+        ov = dict(k_scale=K, w_y=w_y, m_pool=m_pool)
+        runner = sdist.BandRunner(W, H, D, dist, "cpu", compute=False, **ov)
+        b = runner.b
+        runner.own_view(0, "L").copy_(torch.from_numpy(L[b.y0:b.y0 + b.rows]))
+        runner.own_view(0, "R").copy_(torch.from_numpy(R[b.y0:b.y0 + b.rows]))
+        for w in runner.exchange(0):
+            w.wait()
+        Lb, Rb = runner.Lsub[0].numpy(), runner.Rsub[0].numpy()
+        ok_x = np.array_equal(Lb, L[b.sub_y0:b.sub_y0 + b.sub_rows]) and \
+            np.array_equal(Rb, R[b.sub_y0:b.sub_y0 + b.sub_rows])
+        # band compute (oracle on the sub-image) and its own-row summaries
+        p = oracle.params(**ov)
+        r = oracle.pipeline(Lb, Rb, D, p, "fixed", stages=("median", "fill", "out"))
+        s0, ys0 = b.sub_y0 // K, b.y0 // K
+        ys1 = (b.y0 + b.rows) // K if b.y0 + b.rows < H else H // K
+        summ_local = _summaries(r["median"])
+        runner.summ.fill_(-1)
+        runner.summ[ys0:ys1] = torch.from_numpy(summ_local[ys0 - s0:ys1 - s0])
+        runner.reduce_summaries()
+        summ = runner.summ.numpy()
+        # rule (d) from the frame-wide summaries (what stereo_band_finish does)
+        fill, out = r["fill"].copy(), r["out"]
+        hi = min(ys1 + (1 if K == 2 else 0), H // K)
+        patched = [y for y in range(ys0, hi) if summ[y, 0] < 0]
+        for y in patched:
+            fill[y - s0] = _rule_d_value(summ, y)
+        if patched:
+            out = fill if K == 1 else oracle.scale_up(fill, Lb, K, p.t_fill)
+        mine = out[b.top:b.top + b.rows]
         parts = [None] * world
-        dist.all_gather_object(parts, (b.o0, b.o1, mine))
+        dist.all_gather_object(parts, (b.y0, b.rows, mine, ok_x))
         if rank == 0:
-            full = oracle.pipeline(L, R, D, oracle.params(k_scale=K, w_y=w_y), "fixed",
-                                   stages=("out",))["out"]
-            got = np.zeros_like(full)
-            for o0, o1, part in parts:
-                got[o0:o1] = part
-            q.put(bool(np.array_equal(got.view(np.uint32), full.view(np.uint32))))
+            full = oracle.pipeline(L, R, D, p, "fixed", stages=("median", "out"))
+            got = np.zeros_like(full["out"])
+            for y0, rows, part, _ in parts:
+                got[y0:y0 + rows] = part
+            ok_summ = np.array_equal(summ, _summaries(full["median"]))
+            q.put((all(pt[3] for pt in parts), bool(ok_summ),
+                   bool(np.array_equal(got.view(np.uint32), full["out"].view(np.uint32)))))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world,case", [
-    (2, (160, 120, 32, 2, 31, "scene")),
-    (3, (96, 150, 24, 1, 7, "scene")),
-    (2, (24, 60, 16, 1, 3, "noise")),
-    (3, (20, 62, 20, 2, 4, "noise")),
-    (3, (10, 90, 16, 2, 1, "noise")),  # rows 26..30 have no GCP: only the global patch is right
+    (2, (160, 120, 32, 2, 31, 1, "scene")),
+    (3, (96, 150, 24, 1, 7, 1, "scene")),
+    (2, (24, 60, 16, 1, 3, 1, "noise")),
+    (3, (20, 62, 20, 2, 4, 1, "noise")),
+    (3, (10, 90, 16, 2, 1, 1, "noise")),   # rows 26..30 have no GCP: only the global patch is right
+    # every pool radius (m_pool = 0 left the band one scaled row short)
+    (3, (64, 96, 16, 2, 4, 0, "scene")),
+    (3, (64, 96, 16, 2, 4, 2, "scene")),
+    (2, (64, 97, 16, 2, 4, 3, "scene")),
+    (3, (40, 96, 16, 2, 4, 0, "noise")),
 ])
 def test_bands_equal_full_frame(world, case):
     import torch.multiprocessing as mp
@@ -100,31 +125,43 @@ def test_bands_equal_full_frame(world, case):
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    assert q.get(timeout=10)
+    ok_x, ok_summ, ok_out = q.get(timeout=10)
+    assert ok_x, "halo exchange delivered wrong rows"
+    assert ok_summ, "all-reduced summaries differ from the frame's"
+    assert ok_out, "assembled bands differ from the full frame"
 
 
-def test_band_plan_covers_and_aligns():
-    for H, P, K in ((992, 8, 2), (991, 3, 2), (375, 4, 1), (1984, 8, 2)):
-        bands = sdist.band_plan(H, P, K)
-        assert bands[0].o0 == 0 and bands[-1].o1 == H
+def test_band_partition_covers_and_aligns():
+    for H, P, K, m in ((992, 8, 2, 1), (991, 3, 2, 1), (375, 4, 1, 1), (1984, 8, 2, 1), (96, 3, 2, 0)):
+        p = abi.default_params(k_scale=K, m_pool=m)
+        bands = sdist.band_layout(H, P, p)
+        assert bands[0].y0 == 0 and bands[-1].y0 + bands[-1].rows == H
         for a, b in zip(bands, bands[1:]):
-            assert a.o1 == b.o0 and a.ys1 == b.ys0
+            assert a.y0 + a.rows == b.y0
         for b in bands:
-            assert b.r0 % K == 0 and b.r0 <= b.o0 and b.r1 >= b.o1
-    with pytest.raises(ValueError):
-        sdist.band_plan(10, 8, 2)
+            assert b.sub_y0 % K == 0 and b.sub_y0 >= 0 and b.sub_y0 + b.sub_rows <= H
+            # the cone: w_y + census reach + cross-check/median/Step8 rows, in scaled rows
+            # (clipped at the frame's edges)
+            assert b.top >= min(b.y0, K * (31 + 2 + 1) + (m if K == 2 else 0))
+            assert b.bot >= min(H - b.y0 - b.rows, K * (31 + 2 + 1 + (K == 2)))
+    with pytest.raises(abi.StereoError):
+        abi.band_rows(10, 8, 0, k_scale=2)
+    with pytest.raises(abi.StereoError):  # odd start for K = 2
+        abi.band_halo(992, 3, 100, k_scale=2)
 
 
-def test_rule_d_patch_values():
-    # rows 0..5: valid at 1 (values 3/7) and 4 (values 9/2)
-    has = np.array([0, 1, 0, 0, 1, 0])
-    first = np.array([-1, 3, -1, -1, 9, -1])
-    last = np.array([-1, 7, -1, -1, 2, -1])
-    b = sdist.Band(0, 0, 6, 0, 6, 0, 6)
-    rows, vals = sdist.rule_d_patches(np.stack([has, first, last]), b, 1, 6)
-    assert rows.tolist() == [0, 2, 3, 5] and vals.tolist() == [3.0, 7.0, 7.0, 2.0]
-    none = sdist.rule_d_patches(np.zeros((3, 4), int), sdist.Band(0, 0, 4, 0, 4, 0, 4), 1, 4)
-    assert none[1].tolist() == [0.0] * 4
+def test_halo_sends_cover_every_sub_image():
+    p = abi.default_params()
+    bands = sdist.band_layout(992, 8, p)
+    sends = sdist.halo_sends(bands)
+    for b in bands:
+        got = set(range(b.y0, b.y0 + b.rows))
+        for src, dst, r0, r1 in sends:
+            if dst == b.rank:
+                got |= set(range(r0, r1))
+        assert got == set(range(b.sub_y0, b.sub_y0 + b.sub_rows))
+    # neighbours only at c3 / 8 bands (the cone is smaller than a band)
+    assert all(abs(s - d) == 1 for s, d, _, _ in sends)
 
 
 def test_stream_slices_partition():

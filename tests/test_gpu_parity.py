@@ -353,14 +353,24 @@ def test_depth_eq1_bit_exact():
     st.close()
 
 
-def test_disparity_maps_vs_double_definition():
+@pytest.mark.parametrize("case", [(450, 375, 64, 1, 2), (300, 200, 48, 2, 5), (160, 120, 32, 1, 9)])
+def test_disparity_maps_vs_double_definition(case):
     """<= 0.01% of D^L/D^R pixels may differ from the double-mode oracle, and
-    only where the two candidates' double costs tie within 1e-5 (north_star)."""
-    L, R, _ = synth.scene(450, 375, 64, seed=2)
-    got = _run_gpu(L, R, 64, k_scale=1)
-    dbl = oracle.pipeline(L, R, 64, oracle.params(k_scale=1), "double", stages=("DL", "DR"))
-    for m in ("DL", "DR"):
-        assert (got[m] != dbl[m]).mean() <= 1e-4
+    every one of them only where the two candidates' double costs tie within
+    1e-5 relative (north_star; the quantisation bound 0.5*2^-f/c_AD(1) per
+    term)."""
+    W, H, D, K, seed = case
+    L, R, _ = synth.scene(W, H, D, seed=seed)
+    got = _run_gpu(L, R, D, k_scale=K)
+    dbl = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "double",
+                          stages=("DL", "DR", "caL_d", "caR_d"))
+    for m, vol in (("DL", "caL_d"), ("DR", "caR_d")):
+        diff = got[m] != dbl[m]
+        assert diff.mean() <= 1e-4
+        v = dbl[vol]
+        for y, x in zip(*np.nonzero(diff)):
+            a, b = v[got[m][y, x], y, x], v[dbl[m][y, x], y, x]
+            assert abs(a - b) <= 1e-5 * abs(b), (m, y, x, a, b)
 
 
 # ---------------------------------------------------------------- stage isolation
@@ -465,6 +475,88 @@ def test_batch_host_and_repeat_determinism():
         st.compute(Lb[4], Rb[4], o2, stream=s2)
     s2.synchronize()
     assert np.array_equal(o2.cpu().numpy(), outs[4])
+    st.close()
+
+
+@pytest.mark.parametrize("nb,n,K", [(1, 3, 2), (3, 7, 2), (8, 8, 1), (5, 11, 1), (4, 6, 2)])
+def test_batch_capacity_bit_exact(nb, n, K):
+    """stereo_create_batch: one launch sequence per chunk of nb frames (the x
+    and y passes see a chunk as one tall image); every frame bit-exact,
+    including chunk tails and frames that need fill rule (d)."""
+    W, H, D = 61, 47, 16
+    frames = []
+    for i in range(n):
+        if i % 3 == 2:  # unrelated noise: all-invalid rows (rule (d))
+            frames.append(synth.random_pair(W, H, seed=40 + i, levels=256))
+        else:
+            frames.append(synth.scene(W, H, D, seed=40 + i)[:2])
+    st = abi.Stereo(W, H, D, max_frames=nb, k_scale=K)
+    assert st.info.max_frames == nb
+    Lb = torch.from_numpy(np.stack([f[0] for f in frames])).to(DEV)
+    Rb = torch.from_numpy(np.stack([f[1] for f in frames])).to(DEV)
+    out = torch.full((n, H, W), float("nan"), dtype=torch.float32, device=DEV)
+    for _ in range(2):  # twice: the per-frame rule-(d) counters reset themselves
+        st.compute_batch(Lb, Rb, out, n)
+    torch.cuda.synchronize()
+    outs = out.cpu().numpy()
+    for k, (L, R) in enumerate(frames):
+        ref = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "fixed", stages=("out",))["out"]
+        assert np.array_equal(outs[k].view(np.uint32), ref.view(np.uint32)), k
+    st.close()
+
+
+def test_batch_capacity_c3_two_frames():
+    W, H, D = 1436, 992, 145
+    frames = [synth.scene(W, H, D, seed=s)[:2] for s in (21, 22, 23)]
+    st1 = abi.Stereo(W, H, D)
+    st2 = abi.Stereo(W, H, D, max_frames=2)
+    Lb = torch.from_numpy(np.stack([f[0] for f in frames])).to(DEV)
+    Rb = torch.from_numpy(np.stack([f[1] for f in frames])).to(DEV)
+    o1 = torch.zeros((3, H, W), dtype=torch.float32, device=DEV)
+    o2 = torch.ones((3, H, W), dtype=torch.float32, device=DEV)
+    st1.compute_batch(Lb, Rb, o1, 3)
+    st2.compute_batch(Lb, Rb, o2, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(o1.view(torch.int32), o2.view(torch.int32))
+    ref = oracle.pipeline(frames[1][0], frames[1][1], D, oracle.params(), "fixed", stages=("out",))["out"]
+    assert np.array_equal(o2[1].cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    st1.close()
+    st2.close()
+
+
+def test_large_and_small_handles_alive_together():
+    """ADVICE r1: the per-kernel dynamic shared-memory limit is process-wide;
+    a later, smaller handle must not break an earlier, larger one."""
+    big = abi.Stereo(2872, 1984, 290)
+    small = abi.Stereo(200, 120, 32)
+    for st, (W, H, D) in ((big, (2872, 1984, 290)), (small, (200, 120, 32)), (big, (2872, 1984, 290))):
+        L, R, _ = synth.scene(W, H, D, seed=1) if W < 1000 else (None, None, None)
+        if L is None:
+            L = np.random.default_rng(0).integers(0, 256, (H, W), dtype=np.uint8)
+            R = np.roll(L, -20, axis=1)
+        out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+        st.compute(torch.from_numpy(L).to(DEV), torch.from_numpy(R).to(DEV), out)
+        torch.cuda.synchronize()  # a launch failure would raise at the next call
+        assert torch.isfinite(out).all()
+    big.close()
+    small.close()
+
+
+def test_binding_rejects_bad_arguments():
+    st = abi.Stereo(64, 48, 16, k_scale=1)
+    L = torch.zeros((48, 64), dtype=torch.uint8, device=DEV)
+    out = torch.zeros((48, 64), dtype=torch.float32, device=DEV)
+    with pytest.raises(ValueError):
+        st.compute(L.cpu(), L, out)            # host tensor
+    with pytest.raises(ValueError):
+        st.compute(L.float(), L, out)          # dtype
+    with pytest.raises(ValueError):
+        st.compute(L[:40], L, out)             # shape
+    with pytest.raises(ValueError):
+        st.compute(L, L, out.double())
+    with pytest.raises(ValueError):
+        st.compute_host(np.zeros((48, 64), np.uint8), np.zeros((48, 64), np.uint8),
+                        np.zeros((48, 63), np.float32))
     st.close()
 
 
