@@ -45,6 +45,10 @@ WORKLOAD_NAME = WORKLOADS["c3"][4]
 METRIC = "fps and Gdisp-evals/s at 1436×992 D=145, 1/2/4/8 B200; % HBM peak"
 PAPER_FPS = 40.0  # GTX 780 Ti, Adirondack(H) 1436x992, Dmax=145
 POOL = 64
+C4_FRAMES = 256  # BASELINE config c4: a stream of 256 frames split across the GPUs
+# frames in flight (streams) and frames per launch sequence (batch capacity)
+# per workload, measured best with tools/tp_batch.py on one B200
+DEFAULT_STREAMS_BATCH = {"c1": (4, 64), "c2": (4, 2), "c3": (4, 2), "c4": (4, 2)}
 
 
 def _peaks():
@@ -205,11 +209,28 @@ def run_reference(args):
     return 0
 
 
+def _source_sha():
+    """Digest of the kernel sources + build flags: ties an ncu capture to the
+    code being benched (profiles/ncu_traffic.json carries the one it saw)."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2212_00488_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(csrc, f), "rb") as fh:
+                h.update(f.encode() + b"\0" + fh.read())
+    import __graft_entry__ as ge
+    h.update(" ".join(ge.NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2212_00488_b200 import abi
+    from paper_2212_00488_b200 import dist as sdist
+    from paper_2212_00488_b200 import synth
 
     ws, rank, local = _dist()
     if ws != args.gpus:
@@ -227,13 +248,31 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
     rdev = torch.device("cpu") if backend == "gloo" else dev  # device of the reduced scalars
     NS = max(1, args.streams)
-    handles = [abi.Stereo(W, H, D, k_scale=K) for _ in range(NS)]  # one handle per stream (not re-entrant)
-    st = handles[0]
-    info = st.info
-    frames = _frames(POOL, seed=1000 + rank)
+    NB = max(1, args.batch)
+    # one handle per stream (not re-entrant), each serving NB frames per launch sequence
+    handles = [abi.Stereo(W, H, D, k_scale=K, max_frames=NB) for _ in range(NS)]
+    info = handles[0].info
+    if args.workload == "c4":  # this rank's contiguous slice of the 256-frame stream
+        sl = sdist.stream_slice(C4_FRAMES, ws, rank)
+        frames = synth.stream(W, H, D, C4_FRAMES, seed=1000, idx=sl)
+        pool_desc = f"frames {sl.start}..{sl.stop - 1} of a {C4_FRAMES}-frame synth.stream (dist.stream_slice)"
+    else:
+        frames = _frames(POOL, seed=1000 + rank)
+        pool_desc = f"{POOL}-frame pool"
+    npool = len(frames)
     Lp = torch.from_numpy(np.stack([f[0] for f in frames])).to(dev)
     Rp = torch.from_numpy(np.stack([f[1] for f in frames])).to(dev)
-    out = torch.empty((NS, H, W), dtype=torch.float32, device=dev)
+    # a chunk = NB consecutive pool frames (wrapping): gathered once into
+    # per-chunk contiguous buffers so that the timed loop only launches
+    nchunk = max(1, npool // NB) if NB > 1 else npool
+    if NB > 1:
+        sel = [[(c * NB + j) % npool for j in range(NB)] for c in range(nchunk)]
+        Lc = [Lp[idx].contiguous() for idx in sel]
+        Rc = [Rp[idx].contiguous() for idx in sel]
+    else:
+        Lc = [Lp[i:i + 1] for i in range(npool)]
+        Rc = [Rp[i:i + 1] for i in range(npool)]
+    out = torch.empty((NS, NB, H, W), dtype=torch.float32, device=dev)
     main = torch.cuda.current_stream(dev)
     streams = [main] + [torch.cuda.Stream(dev) for _ in range(NS - 1)]
 
@@ -241,20 +280,27 @@ def run_ours(args):
         if ws > 1:
             dist.barrier()
 
-    def step(i, ns=NS):
-        k = i % ns
-        handles[k].compute(Lp[i % POOL], Rp[i % POOL], out[k], stream=streams[k])
+    def run_frames(n, ns, c0=0):
+        """n frames as chunks of NB, chunk c on stream c % ns (the last chunk may be short)."""
+        c, done = c0, 0
+        while done < n:
+            k = c % ns
+            m = min(NB, n - done)
+            handles[k].compute_batch(Lc[c % nchunk][:m], Rc[c % nchunk][:m], out[k][:m], m,
+                                     stream=streams[k])
+            done += m
+            c += 1
+        return c
 
-    def timed(nsteps, ns):
-        """Device time of nsteps frames round-robin over ns streams (events on
-        the main stream; the other streams are forked from / joined into it)."""
+    def timed(nframes, ns, c0=0):
+        """Device time of nframes frames over ns streams (events on the main
+        stream; the other streams fork from / join into it)."""
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ends = [torch.cuda.Event() for _ in range(ns)]
         e0.record(main)
         for s_ in streams[1:ns]:
             s_.wait_event(e0)
-        for i in range(nsteps):
-            step(args.warmup + i, ns)
+        run_frames(nframes, ns, c0)
         for k in range(1, ns):
             ends[k].record(streams[k])
             main.wait_event(ends[k])
@@ -262,21 +308,21 @@ def run_ours(args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
-    for i in range(args.warmup):
-        step(i)
+    run_frames(max(args.warmup, 2 * NS * NB), NS)
     torch.cuda.synchronize()
-    ms_single = timed(min(args.steps, 500), 1) / min(args.steps, 500)  # one stream, for reference
+    nsingle = min(args.steps, 500)
+    ms_single = timed(nsingle, 1) / nsingle  # one stream, for reference
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms_total = timed(args.steps, NS)
+        ms_total = timed(args.steps, NS, c0=1)
     barrier()
     torch.cuda.synchronize()
     # per-kernel device time for the roofline: CUDA events recorded around every
-    # stage on the launch stream, over a second timed pass of the same frames
+    # stage on the launch stream (one stream, launches of NB frames each)
+    st = handles[0]
     st.set_timing(True)
-    for i in range(min(args.steps, 512)):
-        step(args.warmup + i, 1)  # one stream: per-kernel times without overlap
+    run_frames(max(NB, min(args.steps, 512) // NB * NB), 1)
     torch.cuda.synchronize()
     stage_ms, nfr = st.stage_times_ms()
     st.set_timing(False)
@@ -287,20 +333,19 @@ def run_ours(args):
     fps = ws * args.steps / (ms_max / 1e3)
 
     # ---- end to end through the public C ABI with HOST buffers (pinned):
-    # H2D of L, R + compute + D2H of the disparity map, every step, on
-    # --e2e-streams handles / streams (at least the device-resident count) so
-    # the copies overlap other frames' kernels.
+    # H2D of L, R + compute + D2H of the disparity map, every frame, on NE
+    # handles / streams so the copies overlap other frames' kernels; at least
+    # 8 frames per stream whatever --steps is (a throughput, not a latency)
     NE = max(NS, args.e2e_streams, 2)
-    extra = [abi.Stereo(W, H, D, k_scale=K) for _ in range(NE - NS)]
-    e2e_h = list(handles) + extra
+    e2e_h = [abi.Stereo(W, H, D, k_scale=K) for _ in range(NE)]
     e2e_s = [torch.cuda.Stream(dev) for _ in range(NE)]
-    nh = 8
+    nh = min(8, npool)
     Lh = [torch.from_numpy(frames[i][0]).pin_memory() for i in range(nh)]
     Rh = [torch.from_numpy(frames[i][1]).pin_memory() for i in range(nh)]
-    Oh = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in range(nh)]
-    e2e_steps = max(args.steps // 4, 8)
+    Oh = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in range(NE)]
+    e2e_steps = max(args.steps, 8 * NE, 64)
     for i in range(2 * NE):
-        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i % NE])
+        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % NE], stream=e2e_s[i % NE])
     torch.cuda.synchronize()
     barrier()
     ea = [torch.cuda.Event(enable_timing=True) for _ in range(NE)]
@@ -309,7 +354,7 @@ def run_ours(args):
     for s_ in range(NE):
         ea[s_].record(e2e_s[s_])
     for i in range(e2e_steps):
-        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % nh], stream=e2e_s[i % NE])
+        e2e_h[i % NE].compute_host(Lh[i % nh], Rh[i % nh], Oh[i % NE], stream=e2e_s[i % NE])
     for s_ in range(NE):
         eb[s_].record(e2e_s[s_])
     torch.cuda.synchronize()
@@ -319,43 +364,48 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_fps = ws * e2e_steps / (float(t2.item()) / 1e3)
-    for h_ in extra:
+    for h_ in e2e_h:
         h_.close()
 
     if rank == 0:
         peak, peak_src = _peaks()
-        # dominant kernel by share of the step
-        dom = max(("XPASS", "YPASS"), key=lambda k: stage_ms[k])
         n = info.Ws * info.Hs
-        vol = info.Ds * n * 4  # one base's CA_x (u32)
-        if dom == "YPASS":
-            alg = 2 * vol + 2 * n * 4 + 2 * n  # read CA_x both bases + arms; write D^L, D^R
-        else:
-            alg = 2 * vol + 2 * n * 2 + 2 * n * 4  # write CA_x both bases; read pix + arms
-        avg_ms = stage_ms[dom] / max(nfr, 1)
+        vol = info.Ds * n * 4  # one base's CA_x (u32), one frame
+        # algorithmic bytes per frame of each aggregation kernel
+        algb = {"xpass": 2 * vol + 2 * n * 2 + 2 * n * 4, "ypass": 2 * vol + 2 * n * 4 + 2 * n}
+        dom = max(("XPASS", "YPASS"), key=lambda k: stage_ms[k])
+        launches = max(nfr // NB, 1)  # launches of the timing pass (NB frames each)
+        avg_ms = stage_ms[dom] / launches
+        alg = algb[dom.lower()] * NB  # per launch
         achieved = alg / (avg_ms / 1e3) / 1e9
-        traffic, prof = None, {}
+        # ncu DRAM traffic / pipe use: from the committed capture, only if it
+        # was taken of these sources (else null, with the reason)
+        traffic, prof, prov = None, {}, None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        sha = _source_sha()
         if os.path.exists(tp):
             try:
                 prof = json.load(open(tp))
-                traffic = prof.get(dom.lower())
             except Exception:
-                traffic, prof = None, {}
+                prof = {}
+            if prof.get("source_sha") == sha:
+                traffic = prof.get(dom.lower())
+                prov = f"ncu --set full capture of these sources ({sha})"
+            else:
+                prov = (f"stale: profiles/ncu_traffic.json is of sources {prof.get('source_sha')}, "
+                        f"these are {sha}")
+                prof = {}
         pipes = prof.get("pipes", {})
-        # both aggregation kernels (north_star: "% HBM peak on the aggregation
-        # kernels" + their INT/ALU/LSU pipe use): algorithmic bytes / live
-        # single-stream kernel time, and the ncu pipe utilisation of one capture
-        algb = {"xpass": 2 * vol + 2 * n * 2 + 2 * n * 4, "ypass": 2 * vol + 2 * n * 4 + 2 * n}
         aggregation = {}
         for k in ("xpass", "ypass"):
-            us = stage_ms[k.upper()] / max(nfr, 1) * 1e3
-            gbs = algb[k] / (us / 1e6) / 1e9
+            us = stage_ms[k.upper()] / launches * 1e3
+            gbs = algb[k] * NB / (us / 1e6) / 1e9
             ncu = pipes.get(k) or {}
             ncu_frac = None
             if prof.get(k) and ncu.get("duration_ns"):  # DRAM bytes / ncu time / peak
                 ncu_frac = prof[k] / (ncu["duration_ns"] * 1e-9) / 1e9 / peak
-            aggregation[k] = {"us": us, "algorithmic_bytes": algb[k], "hbm_gbs": gbs,
+            aggregation[k] = {"us_per_launch": us, "frames_per_launch": NB,
+                              "algorithmic_bytes_per_launch": algb[k] * NB, "hbm_gbs": gbs,
                               "hbm_frac": gbs / peak, "ncu_dram_hbm_frac": ncu_frac,
                               "ncu_pipes": pipes.get(k)}
         step_ms = ms_max / args.steps
@@ -365,20 +415,20 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": fps / PAPER_FPS if (W, H, D) == (1436, 992, 145) else None,
             "dtype": "u32/u64 fixed-point (f32 fill/scale-up)", "data": "synthetic",
             "config": {"workload": WORKLOAD_NAME + ", 1 frame per GPU per step",
-                       "frames_pool": POOL,
-                       "l2": f"inputs larger than L2: {POOL}-frame pool "
-                             f"({POOL * W * H * 2 / 1e6:.0f} MB) + {2 * vol / 1e6:.0f} MB CA_x "
-                             "written and read per frame",
+                       "frames": pool_desc,
+                       "l2": f"inputs larger than L2: {npool * W * H * 2 / 1e6:.0f} MB of frames + "
+                             f"{2 * vol / 1e6:.0f} MB CA_x written and read per frame",
                        "parallelism": f"frame-batch dp{ws}" if ws > 1 else "single GPU",
-                       "streams_per_gpu": NS, "e2e_streams_per_gpu": NE,
+                       "streams_per_gpu": NS, "frames_per_launch": NB, "e2e_streams_per_gpu": NE,
                        "ms_per_step_single_stream": ms_single},
             "gdisp_evals_per_s": fps * W * H * D / 1e9,
             "executed_gdisp_evals_per_s": fps * 2 * info.Ws * info.Hs * info.Ds / 1e9,
-            "stage_us": {k: v / max(nfr, 1) * 1e3 for k, v in stage_ms.items()},
+            "stage_us_per_frame": {k: v / max(nfr, 1) * 1e3 for k, v in stage_ms.items()},
             "roofline": {"kernel": dom.lower(), "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg, "pipes": pipes.get(dom.lower())},
+                         "traffic": traffic * NB if traffic else None, "traffic_source": prov,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                         "frames_per_launch": NB, "pipes": pipes.get(dom.lower())},
             "aggregation_kernels": aggregation,
             # the measured bound of the dominant kernel: its
             # shared-memory port, 1 wavefront (128 B) per SM per cycle
@@ -386,14 +436,14 @@ def run_ours(args):
                                "achieved": pipes[dom.lower()]["smem_wavefronts_per_sm_cycle"],
                                "peak": 1.0, "unit": "wavefronts/SM/cycle",
                                "frac": pipes[dom.lower()]["smem_wavefronts_per_sm_cycle"],
-                               "source": "ncu --set full (profiles/ncu_traffic.json)"}
+                               "source": prov}
                               if pipes.get(dom.lower(), {}).get("smem_wavefronts_per_sm_cycle") else None),
             "cpu_baseline": _cpu_baseline() if ws == 1 else None,
             "e2e": {"value": e2e_fps, "unit": "fps", "h2d_bytes_per_step": 2 * W * H,
                     "d2h_bytes_per_step": 4 * W * H, "steps": e2e_steps,
                     "how": "stereo_compute_host (pinned host L/R -> device, compute, device -> host "
                            f"f32 map), {NE} handles on {NE} streams", "wall_s": wall},
-            "gpu_launches": args.steps * info.launches_per_frame,
+            "gpu_launches": -(-args.steps // NB) * info.launches_per_frame,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
@@ -500,15 +550,21 @@ def main():
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c3",
                     help="c3 (default, the driver's leg) and c1 / c2 / c4: frame batches; "
                          "c5: one high-res frame per step in row bands across the ranks")
-    ap.add_argument("--streams", type=int, default=4,
-                    help="frames in flight per GPU (one handle per stream); measured "
-                         "best of 2..8 at c3: 4")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="launch sequences in flight per GPU (one handle per stream); "
+                         "0 = the workload's measured best (DEFAULT_STREAMS_BATCH)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="frames per launch sequence (stereo_create_batch); 0 = the "
+                         "workload's measured best")
     ap.add_argument("--e2e-streams", type=int, default=8,
                     help="frames in flight for the end-to-end (host buffer) leg: the "
                          "copies need more overlap (6 / 8 / 12 measured: 7.60 / 7.75 / 7.76 k fps)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ns, nb = DEFAULT_STREAMS_BATCH.get(args.workload, (4, 1))
+    args.streams = args.streams or ns
+    args.batch = args.batch or nb
     global W, H, D, K, WORKLOAD_NAME
     if args.workload in WORKLOADS:
         W, H, D, K, WORKLOAD_NAME = WORKLOADS[args.workload]

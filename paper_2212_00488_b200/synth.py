@@ -109,19 +109,24 @@ def scene(W: int, H: int, D: int, seed: int = 0, view_noise: int = 2):
     return L, R, dgt
 
 
-def stream(W: int, H: int, D: int, n: int, seed: int = 0, view_noise: int = 2):
-    """n frames (L, R) of one scene translating 1..3 px/frame; list of tuples."""
+def stream(W: int, H: int, D: int, n: int, seed: int = 0, view_noise: int = 2, idx=None):
+    """n frames (L, R) of one scene translating 1..3 px/frame; list of tuples.
+
+    idx: the frame indices to render (default: all n).  Every frame draws its
+    own noise from a generator keyed by (seed, frame), so a rank renders just
+    its slice of the stream (config c4, dist.stream_slice) and gets the same
+    frames as a whole-stream render."""
     rng = np.random.default_rng(seed)
     T = patchy(W, H, rng, noise=0)
     fresh = patchy(W, H, rng, noise=0)
     dgt = _disparity_field(W, H, D, rng)
+    offs = np.concatenate([[0], np.cumsum(rng.integers(1, 4, max(n - 1, 0)))]).astype(int)
     frames = []
-    off = 0
-    for _ in range(n):
+    for i in (range(n) if idx is None else idx):
+        off = int(offs[i])
         Ts = np.roll(T, off, axis=1)
         ds = np.roll(dgt, off, axis=1)
-        frames.append(_render(Ts, ds, fresh, rng, view_noise))
-        off += int(rng.integers(1, 4))
+        frames.append(_render(Ts, ds, fresh, np.random.default_rng([seed, 7, i]), view_noise))
     return frames
 
 
