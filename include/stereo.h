@@ -91,7 +91,8 @@ typedef struct {
   int32_t device;         /* CUDA device ordinal the handle is bound to */
   uint64_t device_bytes;  /* total device scratch owned by the handle */
   uint64_t cax_bytes;     /* bytes of ONE CA_x volume (u32 [ceil(Ds/2)][Hs][cax_pitch][2]) */
-  int32_t launches_per_frame; /* kernels enqueued by one stereo_compute */
+  int32_t launches_per_frame; /* kernels enqueued by one launch sequence (one
+                                 stereo_compute, or one chunk of max_frames frames) */
   int32_t ypass_block_rows;   /* output rows per y-aggregation tile */
   int32_t cax_pitch;          /* row pitch (elements) of the CA_x volumes */
   /* ABI 3 */

@@ -38,9 +38,11 @@ int fail(int code, const char* fmt, ...) {
                   "%s: %s", #call, cudaGetErrorString(e_));                      \
   } while (0)
 
+constexpr int kMaxMarks = 140;  // launches per sequence (L2 band staging: 2 per band)
+
 struct TimedFrame {
-  cudaEvent_t ev[STEREO_STAGE_COUNT + 1];
-  int stage[STEREO_STAGE_COUNT];
+  cudaEvent_t ev[kMaxMarks + 1];
+  int stage[kMaxMarks];
   int n;
   int frames;  // frames of this launch sequence (a batch chunk)
 };
@@ -66,6 +68,7 @@ struct stereo_s {
   stereo_params params{};
   int device = 0;
   bool debug_ca = false;
+  int l2_tail0 = -1, l2_tail1 = -1;  // L2 band staging: CA_x rows still to discard
   uint32_t qad_h[256];
   uint32_t qmc_h[7];
   std::vector<void*> allocs;
@@ -206,10 +209,34 @@ int enqueue_frames(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, 
   const bool padded = (Ls == b.Ls && Rs == b.Rs) || (Ls == b.grayL && Rs == b.grayR);
   CU(launch_prep(g, h->plan, Ls, Rs, padded, b, nfr, s));
   mark(STEREO_STAGE_PREP);
-  CU(launch_xpass(g, h->plan, b, nfr, s));
-  mark(STEREO_STAGE_XPASS);
-  CU(launch_ypass(g, h->plan, b, h->debug_ca, nfr, s));
-  mark(STEREO_STAGE_YPASS);
+  const Plan& p = h->plan;
+  if (p.l2_bands > 1 && !h->debug_ca) {
+    // L2 band staging (NEXT-1 prototype): x pass of band k's
+    // rows (+ w_y rows ahead), then the y pass of band k's outputs, which
+    // reads CA_x rows written moments before (L2 hits); rows no later band
+    // reads are discarded from L2 by the next x-pass launch (no write-back)
+    const int R = nfr * g.Hs, Bb = p.l2_band_rows, wy = g.w_y;
+    for (int k = 0, xa = 0; k * Bb < R; ++k) {
+      const int xb = std::min(R, (k + 1) * Bb + wy);
+      int d0 = std::max(0, (k - 1) * Bb - wy), d1 = std::max(0, k * Bb - wy);
+      if (k == 0) {  // the previous frame's tail, when disjoint from the rows written now
+        d0 = d1 = 0;
+        if (h->l2_tail0 >= xb && h->l2_tail1 > h->l2_tail0) { d0 = h->l2_tail0; d1 = h->l2_tail1; }
+      }
+      if (xb > xa || d1 > d0) CU(launch_xpass_rows(g, p, b, xa, xb - xa, d0, d1, s));
+      mark(STEREO_STAGE_XPASS);
+      xa = xb;
+      CU(launch_ypass_rows(g, p, b, k * Bb, std::min(R, (k + 1) * Bb), s));
+      mark(STEREO_STAGE_YPASS);
+      h->l2_tail0 = std::max(0, k * Bb - wy);
+      h->l2_tail1 = R;
+    }
+  } else {
+    CU(launch_xpass(g, p, b, nfr, s));
+    mark(STEREO_STAGE_XPASS);
+    CU(launch_ypass(g, p, b, h->debug_ca, nfr, s));
+    mark(STEREO_STAGE_YPASS);
+  }
   CU(launch_post(g, h->plan, b, L, out, nfr, s));
   mark(STEREO_STAGE_POST);
   if (h->timing) {
@@ -564,7 +591,11 @@ int stereo_get_info(const stereo_t* h, stereo_info* info) {
   const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * g.Wp;  // disparity pairs (u32 x 2)
   info->device_bytes = h->bytes + (h->b.caL ? 2 * (size_t)g.Ds * g.Hs * g.Ws * 8 : 0);
   info->cax_bytes = vol * 4;
-  info->launches_per_frame = g.K == 2 ? 5 : 4;
+  {
+    const Plan& p = h->plan;
+    const int agg = p.l2_bands > 1 ? 2 * ((g.NB * g.Hs + p.l2_band_rows - 1) / p.l2_band_rows) : 2;
+    info->launches_per_frame = (g.K == 2 ? 3 : 2) + agg;  // per launch sequence (max_frames frames)
+  }
   info->ypass_block_rows = h->plan.ypass_B;
   info->cax_pitch = g.Wp;
   info->max_frames = g.NB;
@@ -614,6 +645,7 @@ int stereo_set_debug(stereo_t* h, int what, int enable) {
   if (what != STEREO_DEBUG_CA) return fail(STEREO_EINVAL, "unknown debug switch %d", what);
   if (h->g.NB != 1) return fail(STEREO_EINVAL, "stage access needs a handle of batch capacity 1");
   DeviceGuard dg(h->device);
+  h->l2_tail0 = h->l2_tail1 = -1;
   if (enable && !h->b.caL) {
     const size_t bytes = (size_t)h->g.Ds * h->g.Hs * h->g.Ws * 8;
     CU(cudaMalloc(&h->b.caL, bytes));

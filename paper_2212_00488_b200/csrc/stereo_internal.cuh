@@ -80,10 +80,13 @@ struct Plan {
   bool xpass_fixpl = false;  // PL = 32C + 128 at compile time (small D_s + w_x)
   int xpass_warps = 0;
   int xpass_slots = 3;  // row slots of the bulk-copy ring
+  int ypass_ver = 1;  // 1: 16-column strips, 2 CTAs/SM; 2: 32-column strips, 16 warps (ypass2_kernel)
   int ypass_B = 0;   // output rows per tile (<= 8*kYRPT)
   int ypass_nb = 0;  // tiles per column strip
   int ypass_SEG = 0; // tile rows per warp; TMA box height = 8*SEG
   int ypass_smem = 0;
+  int l2_bands = 0;  // > 1: C+CA_x / CA+WTA interleaved over this many row bands (NEXT-1 prototype)
+  int l2_band_rows = 0;
   CUtensorMap tmL, tmR;  // 3-D u64 maps over the CA_x volumes {Wp, Hs, ceil(Ds/2)}
   int post_smem = 0;
   int post_rows = 2;     // scaled rows per POST CTA
@@ -102,6 +105,13 @@ cudaError_t launch_sd(const Geom& g, const Plan& p, const uint8_t* Lorg, const u
 cudaError_t launch_prep(const Geom& g, const Plan& p, const uint8_t* Ls, const uint8_t* Rs, bool padded,
                         Buffers& b, int nfr, cudaStream_t s);
 cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, int nfr, cudaStream_t s);
+// rows [row0, row0 + rows) of the batch image only; first discards rows
+// [disc0, disc1) of both CA_x volumes from L2 (L2 band staging)
+cudaError_t launch_xpass_rows(const Geom& g, const Plan& p, Buffers& b, int row0, int rows,
+                              int disc0, int disc1, cudaStream_t s);
+// output rows [y0, y1) of the batch image only (L2 band staging)
+cudaError_t launch_ypass_rows(const Geom& g, const Plan& p, Buffers& b, int y0, int y1,
+                              cudaStream_t s);
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca, int nfr,
                          cudaStream_t s);
 // band mode: out = the caller's band output (own original rows only)

@@ -739,6 +739,146 @@ __global__ void __launch_bounds__(kYThreads, 2)
     if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(__double2loint(best[r]) & 255);
 }
 
+// Wide-strip variant (v2): CTA = 32-column strip x B output rows, 16 warps,
+// warp w = tile row segment w (SEG rows) across all 32 columns.  Every warp
+// access of the prefix arrays then lies in ONE tile row (32 consecutive
+// columns): the hi prefixes (4 B per column) are one conflict-free wavefront
+// per access instead of the two half-warps' rows meeting in the same bank half
+// (v1: ~20% of the y pass's wavefronts were such conflicts).  Same arithmetic,
+// same layouts, same WTA as v1; the segment offsets come from the earlier
+// warps' column totals (independent loads, issued back to back).
+constexpr int kY2Threads = 512;
+constexpr int kY2Cols = 32;
+
+template <int SEG, bool DBG>
+__global__ void __launch_bounds__(kY2Threads, 1)
+    ypass2_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                  YArgs a) {
+  constexpr int TB = kYSegs * SEG;                        // tile rows = TMA box height
+  constexpr uint32_t kTileBytes = 2 * TB * kY2Cols * 4;   // box {32 columns, TB rows, 1 pair} of u64
+  extern __shared__ __align__(128) uint8_t ysm[];
+  uint32_t* tile = reinterpret_cast<uint32_t*>(ysm);                          // [kYStages][TB][32] x u64
+  uint2* Elo = reinterpret_cast<uint2*>(ysm + kYStages * kTileBytes);          // [TB+1][32]
+  uint32_t* Ehi = reinterpret_cast<uint32_t*>(Elo + (TB + 1) * kY2Cols);      // [TB+1][32]
+  uint4* tot = reinterpret_cast<uint4*>(Ehi + (TB + 1) * kY2Cols);            // [16][32]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tot + kYSegs * kY2Cols);        // [kYStages]
+  const int tid = threadIdx.x, col = tid & 31, seg = tid >> 5;
+  const int base = blockIdx.z;
+  const CUtensorMap* tm = base ? &tm1 : &tm0;
+  const uint32_t* armp = base ? a.arm1 : a.arm0;
+  uint8_t* dmap = base ? a.D1 : a.D0;
+  uint64_t* cadbg = base ? a.ca1 : a.ca0;
+  const int x0 = blockIdx.x * kY2Cols, x = x0 + col;
+  const int y0 = a.y_begin + blockIdx.y * a.B, yt0 = y0 - a.w_y;
+  const int Ds = a.Ds;
+  // output rows of this thread: y0 + seg + 16 r, r < nr (warp-uniform)
+  const int nrow = min(a.B, a.y_end - y0);
+  const int nr = max(0, (nrow - seg + 15) >> 4);
+
+  if (tid == 0) {
+    for (int s = 0; s < kYStages; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kYStages && 2 * s < Ds; ++s) {
+      mbar_expect_tx(bar + s, kTileBytes);
+      tma_load_3d(tile + s * 2 * TB * kY2Cols, tm, bar + s, x0, yt0, s);
+    }
+  }
+  __syncthreads();
+  if (tid < kY2Cols) {
+    Elo[tid] = make_uint2(0u, 0u);
+    Ehi[tid] = 0u;
+  }
+  // window byte offsets into Elo (Ehi: half of it), packed a | b << 16
+  // (< 2^16: (TB+1)*32*8 <= 61696), and the running minimum keys
+  uint32_t oab[kYRPT];
+  double best[kYRPT];
+#pragma unroll
+  for (int r = 0; r < kYRPT; ++r) {
+    const int y = y0 + seg + 16 * r;
+    oab[r] = 0u;
+    best[r] = __hiloint2double(0x7ff00000, 0);  // +inf
+    if (r < nr && x < a.Ws) {
+      const uint32_t arm = __ldg(armp + (size_t)y * a.Ws + x);
+      const int M = (arm >> 16) & 255u, N = arm >> 24;
+      oab[r] = (((uint32_t)(y - M - yt0) * kY2Cols + col) * 8u) |
+               ((((uint32_t)(y + N + 1 - yt0) * kY2Cols + col) * 8u) << 16);
+    }
+  }
+  const uint8_t* EloB = reinterpret_cast<const uint8_t*>(Elo);
+  const uint8_t* EhiB = reinterpret_cast<const uint8_t*>(Ehi);
+  uint2* Ew = Elo + (seg * SEG + 1) * kY2Cols + col;
+  uint32_t* Hw = Ehi + (seg * SEG + 1) * kY2Cols + col;
+  constexpr uint32_t kLoMask = (1u << kYSplit) - 1u;
+
+#pragma unroll 1
+  for (int d = 0; d < Ds; d += 2) {
+    const int it = d >> 1, st = it & 1;
+    mbar_wait(bar + st, (it >> 1) & 1);
+    const uint2* t01 = reinterpret_cast<const uint2*>(tile + st * 2 * TB * kY2Cols) + seg * SEG * kY2Cols + col;
+    uint32_t l0[SEG], l1[SEG], lh[SEG];
+    uint32_t a0 = 0, a1 = 0, ah = 0;
+#pragma unroll
+    for (int s = 0; s < SEG; ++s) {
+      const uint2 v = t01[s * kY2Cols];
+      a0 += v.x & kLoMask;
+      a1 += v.y & kLoMask;
+      ah += __byte_perm(v.x, 0u, 0x4443u) + __byte_perm(v.y, 0u, 0x4344u);  // v.x.b3 | v.y.b3 << 16
+      l0[s] = a0; l1[s] = a1; lh[s] = ah;
+    }
+    tot[seg * kY2Cols + col] = make_uint4(a0, a1, ah, 0u);
+    __syncthreads();  // (1) tile[st] consumed, segment totals visible
+    if (tid == 0 && d + 2 * kYStages < Ds) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar + st, kTileBytes);
+      tma_load_3d(tile + st * 2 * TB * kY2Cols, tm, bar + st, x0, yt0, (d >> 1) + kYStages);
+    }
+    uint32_t o0 = 0u, o1 = 0u, oh = 0u;
+#pragma unroll
+    for (int q = 0; q < kYSegs - 1; ++q) {
+      if (q < seg) {  // warp-uniform
+        const uint4 t = tot[q * kY2Cols + col];
+        o0 += t.x; o1 += t.y; oh += t.z;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < SEG; ++s) {
+      Ew[s * kY2Cols] = make_uint2(l0[s] + o0, l1[s] + o1);
+      Hw[s * kY2Cols] = lh[s] + oh;
+    }
+    __syncthreads();  // (2) column prefixes complete
+    if (d + 1 < Ds)
+      ypass_wta_n<true>(nr, best, oab, EloB, EhiB, d, a.e52);
+    else
+      ypass_wta_n<false>(nr, best, oab, EloB, EhiB, d, a.e52);
+    if (DBG) ypass_debug_store(oab, nr, EloB, EhiB, d, d + 1 < Ds, cadbg, a.Hs, a.Ws, y0 + seg, x);
+  }
+#pragma unroll
+  for (int r = 0; r < kYRPT; ++r)
+    if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(__double2loint(best[r]) & 255);
+}
+
+static int ypass2_smem_bytes(int SEG) {
+  const int TB = kYSegs * SEG;
+  return kYStages * 2 * TB * kY2Cols * 4 + (TB + 1) * kY2Cols * 12 + kYSegs * kY2Cols * 16 + kYStages * 8;
+}
+
+#define YPASS2_DISPATCH(S_, EXPR)                      \
+  switch (S_) {                                        \
+    case 4: { constexpr int SS = 4; EXPR; } break;     \
+    case 5: { constexpr int SS = 5; EXPR; } break;     \
+    case 6: { constexpr int SS = 6; EXPR; } break;     \
+    case 7: { constexpr int SS = 7; EXPR; } break;     \
+    case 8: { constexpr int SS = 8; EXPR; } break;     \
+    case 9: { constexpr int SS = 9; EXPR; } break;     \
+    case 10: { constexpr int SS = 10; EXPR; } break;   \
+    case 11: { constexpr int SS = 11; EXPR; } break;   \
+    case 12: { constexpr int SS = 12; EXPR; } break;   \
+    case 13: { constexpr int SS = 13; EXPR; } break;   \
+    case 14: { constexpr int SS = 14; EXPR; } break;   \
+    case 15: { constexpr int SS = 15; EXPR; } break;   \
+    default: break;                                    \
+  }
+
 #define YPASS_DISPATCH(S_, EXPR)                       \
   switch (S_) {                                        \
     case 5: { constexpr int SS = 5; EXPR; } break;     \
@@ -750,8 +890,9 @@ __global__ void __launch_bounds__(kYThreads, 2)
     default: break;                                    \
   }
 
-static int ypass_seg_for(int T) {
+static int ypass_seg_for(int T, int ver) {
   const int need = (T + kYSegs - 1) / kYSegs;
+  if (ver == 2) return need <= 15 ? std::max(need, 4) : 0;
   for (int s : {5, 7, 9, 11, 13, 15})
     if (s >= need) return s;
   return 0;
@@ -764,21 +905,46 @@ static int ypass_smem_bytes(int SEG) {
 
 
 
+static cudaError_t launch_ypass_range(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
+                                      int y_begin, int y_end, cudaStream_t s);
+
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca, int nfr,
                          cudaStream_t s) {
+  // whole frames (the batch as one image of nfr*Hs rows), or in band mode
+  // only the rows whose D^L / D^R the band's POST reads
+  return launch_ypass_range(g, p, b, store_ca, g.band ? g.ya : 0, g.band ? g.yb : nfr * g.Hs, s);
+}
+
+cudaError_t launch_ypass_rows(const Geom& g, const Plan& p, Buffers& b, int y0, int y1,
+                              cudaStream_t s) {
+  return launch_ypass_range(g, p, b, false, y0, y1, s);
+}
+
+static cudaError_t launch_ypass_range(const Geom& g, const Plan& p, Buffers& b, bool store_ca,
+                                      int y_begin, int y_end, cudaStream_t s) {
   YArgs a;
   a.arm0 = b.armL; a.arm1 = b.armR;
   a.D0 = b.DL; a.D1 = b.DR;
   a.ca0 = store_ca ? b.caL : nullptr;
   a.ca1 = store_ca ? b.caR : nullptr;
   a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
-  // whole frames (the batch as one image of nfr*Hs rows), or in band mode
-  // only the rows whose D^L / D^R the band's POST reads
-  a.y_begin = g.band ? g.ya : 0;
-  a.y_end = g.band ? g.yb : nfr * g.Hs;
+  a.y_begin = y_begin;
+  a.y_end = y_end;
   a.e52 = kYExp52;
-  dim3 grid((g.Ws + 15) / 16, (a.y_end - a.y_begin + p.ypass_B - 1) / p.ypass_B, 2);
+  const int cols = p.ypass_ver == 2 ? kY2Cols : 16;
+  dim3 grid((g.Ws + cols - 1) / cols, (a.y_end - a.y_begin + p.ypass_B - 1) / p.ypass_B, 2);
   cudaError_t e = cudaErrorInvalidValue;
+  if (p.ypass_ver == 2) {
+    if (store_ca)
+      YPASS2_DISPATCH(p.ypass_SEG,
+                      (ypass2_kernel<SS, true><<<grid, kY2Threads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
+                       e = cudaGetLastError()))
+    else
+      YPASS2_DISPATCH(p.ypass_SEG,
+                      (ypass2_kernel<SS, false><<<grid, kY2Threads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
+                       e = cudaGetLastError()))
+    return e;
+  }
   if (store_ca)
     YPASS_DISPATCH(p.ypass_SEG,
                    (ypass_kernel<SS, true><<<grid, kYThreads, p.ypass_smem, s>>>(p.tmL, p.tmR, a),
@@ -1393,8 +1559,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // 3-D map over a CA_x volume as u64 elements (the (d, d+1) pair of a pixel):
-// {Wp columns, Hs rows, ceil(Ds/2) pairs}; box {16 columns, box_rows, 1 pair}
-static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_rows) {
+// {Wp columns, Hs rows, ceil(Ds/2) pairs}; box {box_cols columns, box_rows, 1 pair}
+static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_cols, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1407,7 +1573,7 @@ static cudaError_t make_tmap(CUtensorMap* m, void* base, const Geom& g, int box_
   const cuuint64_t rows = (cuuint64_t)g.NB * g.Hs;  // the batch as one tall image
   cuuint64_t dims[3] = {(cuuint64_t)g.Wp, rows, (cuuint64_t)((g.Ds + 1) / 2)};
   cuuint64_t strides[2] = {(cuuint64_t)g.Wp * 8, (cuuint64_t)g.Wp * rows * 8};
-  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1474,8 +1640,21 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   // (per-CTA shared wavefronts per d ~ 1.25*TB + 1.75*B + tot exchange)
   // rows of one launch: a whole batch of NB frames (one tall image), or in
   // band mode the rows whose maps the band's POST reads
-  const int yrows = g.band ? g.yb - g.ya : g.NB * g.Hs;
-  const int strips = (g.Ws + 15) / 16;
+  const int yrows0 = g.band ? g.yb - g.ya : g.NB * g.Hs;
+  // L2 band staging (NEXT-1 prototype, STEREO_L2_BANDS = n > 1): the x and y
+  // passes alternate over n row bands so that a band's CA_x is read back from
+  // L2 and discarded there (never written to HBM); off in band mode
+  p.l2_bands = g.band ? 0 : env_int("STEREO_L2_BANDS", 0, 0, 64);
+  if (p.l2_bands > 1) p.l2_band_rows = (yrows0 + p.l2_bands - 1) / p.l2_bands;
+  else p.l2_bands = 0;
+  const int yrows = p.l2_bands ? p.l2_band_rows : yrows0;
+  // version 1 (16-column strips, two CTAs per SM); STEREO_YPASS_V=2 selects
+  // the 32-column strips (conflict-free prefix reads, one 16-warp CTA per
+  // SM: measured 2.1x slower at c3, 88 -> 183 us); tiles per
+  // strip balance the halo cost against waves
+  p.ypass_ver = env_int("STEREO_YPASS_V", 1, 1, 2);
+  const int cols = p.ypass_ver == 2 ? kY2Cols : 16;
+  const int strips = (g.Ws + cols - 1) / cols;
   const int nb0 = (yrows + kYSegs * kYRPT - 1) / (kYSegs * kYRPT);
   double best = 1e30;
   p.ypass_nb = 0;
@@ -1483,27 +1662,42 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
   for (int nb = nb0; nb <= yrows; ++nb) {
     if (nb_force && nb != nb_force) continue;
     const int B = (yrows + nb - 1) / nb;
-    const int SEG = ypass_seg_for(B + 2 * g.w_y);
+    const int SEG = ypass_seg_for(B + 2 * g.w_y, p.ypass_ver);
     if (!SEG) continue;
-    const int smem = ypass_smem_bytes(SEG);
+    const int smem = p.ypass_ver == 2 ? ypass2_smem_bytes(SEG) : ypass_smem_bytes(SEG);
     const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
     const int ctas = strips * nb * 2;
     const double waves = (double)((ctas + nsm * per_sm - 1) / (nsm * per_sm));
-    const double cost = waves * per_sm * (1.25 * kYSegs * SEG + 1.75 * B + 20.0);
+    // shared-memory wavefronts per CTA and disparity pair (v1 in 16-column
+    // units: tile + split prefix ~1.25 TB, windows ~1.75 B; v2 in 32-column
+    // units: TMA write + read + prefix 7 TB, windows 6 B, segment totals)
+    const double cost = p.ypass_ver == 2 ? waves * (7.0 * kYSegs * SEG + 6.0 * B + 60.0)
+                                         : waves * per_sm * (1.25 * kYSegs * SEG + 1.75 * B + 20.0);
     if (cost < best - 1e-9) {
       best = cost;
       p.ypass_nb = nb; p.ypass_B = B; p.ypass_SEG = SEG; p.ypass_smem = smem;
     }
   }
   if (!p.ypass_nb) return cudaErrorInvalidValue;
-  YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, false>));
-  if (e != cudaSuccess) return e;
-  YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, true>));
-  if (e != cudaSuccess) return e;
-  YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, false>, p.ypass_smem));
-  if (e != cudaSuccess) return e;
-  YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, true>, p.ypass_smem));
-  if (e != cudaSuccess) return e;
+  if (p.ypass_ver == 2) {
+    YPASS2_DISPATCH(p.ypass_SEG, e = max_carveout(ypass2_kernel<SS, false>));
+    if (e != cudaSuccess) return e;
+    YPASS2_DISPATCH(p.ypass_SEG, e = max_carveout(ypass2_kernel<SS, true>));
+    if (e != cudaSuccess) return e;
+    YPASS2_DISPATCH(p.ypass_SEG, e = raise_smem(ypass2_kernel<SS, false>, p.ypass_smem));
+    if (e != cudaSuccess) return e;
+    YPASS2_DISPATCH(p.ypass_SEG, e = raise_smem(ypass2_kernel<SS, true>, p.ypass_smem));
+    if (e != cudaSuccess) return e;
+  } else {
+    YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, false>));
+    if (e != cudaSuccess) return e;
+    YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(ypass_kernel<SS, true>));
+    if (e != cudaSuccess) return e;
+    YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, false>, p.ypass_smem));
+    if (e != cudaSuccess) return e;
+    YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, true>, p.ypass_smem));
+    if (e != cudaSuccess) return e;
+  }
   // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows
   p.xpass_C = xpass_chunk_for(g.Ws);
   if (!p.xpass_C) return cudaErrorInvalidValue;
@@ -1545,8 +1739,9 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     if (e != cudaSuccess) return e;
     p.xpass_grid = nsm;
   }
-  if ((e = make_tmap(&p.tmL, b.caxL, g, kYSegs * p.ypass_SEG))) return e;
-  if ((e = make_tmap(&p.tmR, b.caxR, g, kYSegs * p.ypass_SEG))) return e;
+  const int box_cols = p.ypass_ver == 2 ? kY2Cols : 16;
+  if ((e = make_tmap(&p.tmL, b.caxL, g, box_cols, kYSegs * p.ypass_SEG))) return e;
+  if ((e = make_tmap(&p.tmR, b.caxR, g, box_cols, kYSegs * p.ypass_SEG))) return e;
   return cudaSuccess;
 }
 

@@ -46,6 +46,12 @@ struct XArgs {
   int slots;  // row slots in the ring (2..kXMaxSlots)
   uint32_t mc_mask;  // 63, as a parameter (see the Q_MC address below)
   const uint32_t* qtab;  // the replicated tables as laid out in shared memory (40 KB)
+  // L2 band staging (NEXT-1 prototype): rows [disc0, disc1) of
+  // both whole volumes whose last reader (a y pass) has run are discarded
+  // from L2 (no write-back to HBM) by this launch, before its own items
+  const uint32_t* discL;
+  const uint32_t* discR;
+  int disc0, disc1;
 };
 
 
@@ -150,6 +156,20 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
     bulk_g2s(sQAD, a.qtab, kTabBytes, tabbar);
     for (int k = 0; k < nslot && rfirst + k <= rlast; ++k)
       xpass_load_row(ring + k * 4 * 32 * C, full + k, a, rfirst + k);
+  }
+  if (a.disc1 > a.disc0) {  // overlaps the table and first-row copies in flight
+    const int lpr = a.Wp * 8 / 128;  // 128-B lines per row of one disparity-pair plane
+    const int nrow = a.disc1 - a.disc0;
+    const long long nl = (long long)npairs * nrow * lpr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nl;
+         i += (long long)gridDim.x * blockDim.x) {
+      const int l = (int)(i % lpr);
+      const long long pr = i / lpr;
+      const int r = (int)(pr % nrow), pp = (int)(pr / nrow);
+      const size_t off = (((size_t)pp * a.Hs + a.disc0 + r) * a.Wp * 8) + (size_t)l * 128;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(a.discL) + off) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(a.discR) + off) : "memory");
+    }
   }
   __syncthreads();  // barrier inits visible
   xbar_wait(tabbar, 0u);
@@ -302,10 +322,14 @@ template <int C>
 constexpr int xpass_nd() { return C <= 2 * kXMaxC2 ? 2 : 1; }
 
 template <int C>
-static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, int nfr, cudaStream_t s) {
-  XArgs a{b.xrow, b.qad, b.qmc, b.caxL, b.caxR,
-          g.Ws, g.NB * g.Hs, g.Ds, g.Wp, p.xpass_PL, g.Ds + g.w_x_max, nfr * g.Hs,
-          g.border, p.xpass_slots, 63u, b.qtab};
+static cudaError_t launch_xpass_c(const Geom& g, const Plan& p, Buffers& b, int row0, int rows,
+                                  int disc0, int disc1, cudaStream_t s) {
+  // rows [row0, row0 + rows) of the (batch) image: the row arrays and both
+  // volumes are addressed from row0 on (rows are independent)
+  XArgs a{b.xrow + (size_t)row0 * g.Wp, b.qad, b.qmc, b.caxL + (size_t)row0 * g.Wp * 2,
+          b.caxR + (size_t)row0 * g.Wp * 2, g.Ws, g.NB * g.Hs, g.Ds, g.Wp, p.xpass_PL,
+          g.Ds + g.w_x_max, rows, g.border, p.xpass_slots, 63u, b.qtab,
+          b.caxL, b.caxR, disc0, disc1};
   if (p.xpass_fixpl)
     xpass_kernel<C, xpass_nd<C>(), true><<<p.xpass_grid, p.xpass_warps * 32, p.xpass_smem, s>>>(a);
   else
@@ -361,8 +385,13 @@ static cudaError_t setup_xpass_c(int smem) {
   }
 
 cudaError_t launch_xpass(const Geom& g, const Plan& p, Buffers& b, int nfr, cudaStream_t s) {
+  return launch_xpass_rows(g, p, b, 0, nfr * g.Hs, 0, 0, s);
+}
+
+cudaError_t launch_xpass_rows(const Geom& g, const Plan& p, Buffers& b, int row0, int rows,
+                              int disc0, int disc1, cudaStream_t s) {
   cudaError_t e = cudaErrorInvalidValue;
-  XPASS_DISPATCH(p.xpass_C, e = launch_xpass_c<CC>(g, p, b, nfr, s));
+  XPASS_DISPATCH(p.xpass_C, e = launch_xpass_c<CC>(g, p, b, row0, rows, disc0, disc1, s));
   return e;
 }
 

@@ -560,6 +560,27 @@ def test_binding_rejects_bad_arguments():
     st.close()
 
 
+@pytest.mark.parametrize("nb,case", [(8, (1436, 992, 145, 2)), (3, (200, 120, 32, 2)),
+                                     (5, (160, 100, 24, 1)), (64, (96, 70, 16, 1))])
+def test_l2_band_staging_bit_exact(nb, case, monkeypatch):
+    """NEXT-1 prototype (STEREO_L2_BANDS): the x and y passes alternate over
+    row bands, CA_x rows discarded from L2 once dead; every output bit-exact
+    (the CA_x volumes themselves are then undefined after a frame)."""
+    W, H, D, K = case
+    monkeypatch.setenv("STEREO_L2_BANDS", str(nb))
+    frames = [synth.scene(W, H, D, seed=s)[:2] for s in (31, 32)]
+    st = abi.Stereo(W, H, D, k_scale=K)
+    monkeypatch.delenv("STEREO_L2_BANDS")
+    out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    for _ in range(2):  # twice: the previous frame's tail discard
+        for L, R in frames:
+            st.compute(torch.from_numpy(L).to(DEV), torch.from_numpy(R).to(DEV), out)
+            torch.cuda.synchronize()
+            ref = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "fixed", stages=("out",))["out"]
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    st.close()
+
+
 def test_stage_timers():
     W, H, D = 1436, 992, 145
     L, R, _ = synth.scene(W, H, D, seed=0)
