@@ -1665,7 +1665,8 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     const int SEG = ypass_seg_for(B + 2 * g.w_y, p.ypass_ver);
     if (!SEG) continue;
     const int smem = p.ypass_ver == 2 ? ypass2_smem_bytes(SEG) : ypass_smem_bytes(SEG);
-    const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
+    // v2: one 512-thread CTA per SM (registers); v1: two when shared memory allows
+    const int per_sm = p.ypass_ver == 2 ? 1 : (smem * 2 <= 227 * 1024 ? 2 : 1);
     const int ctas = strips * nb * 2;
     const double waves = (double)((ctas + nsm * per_sm - 1) / (nsm * per_sm));
     // shared-memory wavefronts per CTA and disparity pair (v1 in 16-column

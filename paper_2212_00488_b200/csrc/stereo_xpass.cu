@@ -186,13 +186,8 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
   const int Ws = a.Ws;
   const uint32_t border = a.border;
 
-  // item -> (row y, pair p), row -> (ring slot, lap): one division at the
-  // start, then incremental updates (a warp's items are nw apart, nw < npairs
-  // is not assumed: the row advance is a short loop)
-  int y = (i0 + warp) / npairs, pidx = i0 + warp - y * npairs;
-  int slot = (y - rfirst) % nslot, lap = (y - rfirst) / nslot;
-#pragma unroll 1
-  for (int it = i0 + warp; it < i1; it += nw) {
+  // one item (row y, pair pidx) whose row sits in ring slot `slot`, lap `lap`
+  auto item = [&](int y, int pidx, int slot, int lap) {
     const int d = pidx * ND;
     xbar_wait(full + slot, (uint32_t)lap & 1u);
     const uint32_t* sL = ring + slot * 4 * 32 * C;
@@ -289,6 +284,16 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
       xpass_windows<C, 2>(sAL, sAR, Pb, Pdb, Pb + PLb, Pdb + PLb + 4, outL, outR, lane, 0);
     else
       xpass_windows<C, 1>(sAL, sAR, Pb, Pdb, Pb, Pdb, outL, outR, lane, 0);
+  };
+#ifndef STEREO_RACECHECK
+  // item -> (row y, pair p), row -> (ring slot, lap): one division at the
+  // start, then incremental updates (a warp's items are nw apart, nw < npairs
+  // is not assumed: the row advance is a short loop)
+  int y = (i0 + warp) / npairs, pidx = i0 + warp - y * npairs;
+  int slot = (y - rfirst) % nslot, lap = (y - rfirst) / nslot;
+#pragma unroll 1
+  for (int it = i0 + warp; it < i1; it += nw) {
+    item(y, pidx, slot, lap);
     __syncwarp();
     // ---- release the row slot: the warp finishing the row's last item of
     // this range refills the slot with the row `slots` ahead
@@ -308,6 +313,33 @@ __global__ void __launch_bounds__(kXMaxWarps * 32, 1) xpass_kernel(XArgs a) {
       if (++slot == nslot) { slot = 0; ++lap; }
     }
   }
+#else
+  // Sanitizer build (-DSTEREO_RACECHECK, tools/sanitize.sh): the same items
+  // in rounds of one item per warp (rw <= npairs, so a round spans at most two
+  // rows), a CTA barrier after every round, and the ring refills issued by
+  // thread 0 after that barrier once a row's items are all done -- the
+  // ordering compute-sanitizer's racecheck models.  Identical results.
+  const int rw = min(nw, npairs);
+  int next = rfirst;  // (thread 0) first row whose slot has not been refilled
+#pragma unroll 1
+  for (int base = i0; base < i1; base += rw) {
+    const int it = base + warp;
+    if (warp < rw && it < i1) {
+      const int y = it / npairs;
+      item(y, it - y * npairs, (y - rfirst) % nslot, (y - rfirst) / nslot);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int done_to = min(i1, base + rw);  // every item < done_to is complete
+      while (next + nslot <= rlast && min(i1, (next + 1) * npairs) <= done_to) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        xpass_load_row(ring + ((next - rfirst) % nslot) * 4 * 32 * C, full + (next - rfirst) % nslot, a,
+                       next + nslot);
+        ++next;
+      }
+    }
+  }
+#endif
 }
 
 int xpass_chunk_for(int Ws) {

@@ -593,3 +593,37 @@ def test_stage_timers():
     ms, n = st.stage_times_ms()
     assert n == 3 and all(v > 0 for v in ms.values())
     st.close()
+
+
+def test_racecheck_variant_bit_exact():
+    """The sanitizer build (lib/racecheck, -DSTEREO_RACECHECK: x-pass ring
+    refills ordered by CTA barriers, the edge compute-sanitizer's racecheck
+    models) gives the same bits as the oracle (run in a subprocess that loads
+    that library instead of the product one)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_rc = os.path.join(root, "paper_2212_00488_b200", "lib", "racecheck", "libstereo_b200.so")
+    if not os.path.exists(lib_rc):
+        pytest.skip("racecheck variant not built (STEREO_SKIP_RACECHECK_BUILD)")
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT)
+import oracle
+from paper_2212_00488_b200 import abi, synth
+assert abi.LIB_PATH.endswith("racecheck/libstereo_b200.so")
+for (W, H, D, K) in ((64, 48, 16, 1), (131, 77, 33, 2), (450, 375, 64, 1), (2880, 64, 40, 2)):
+    L, R, _ = synth.scene(W, H, D, seed=3)
+    st = abi.Stereo(W, H, D, k_scale=K)
+    out = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    st.compute(torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda(), out)
+    torch.cuda.synchronize()
+    ref = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "fixed", stages=("out",))["out"]
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32)), (W, H, D, K)
+    st.close()
+print("ok")
+'''.replace("ROOT", repr(root))
+    env = dict(os.environ, STEREO_B200_LIB=lib_rc)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
