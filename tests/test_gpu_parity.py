@@ -627,3 +627,18 @@ print("ok")
     env = dict(os.environ, STEREO_B200_LIB=lib_rc)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("case", [(1436, 992, 145, 2), (300, 200, 48, 1)])
+def test_ypass_v2_wide_strips_bit_exact(case, monkeypatch):
+    """The 32-column y pass (STEREO_YPASS_V=2, a measured-slower experiment
+    kept selectable) gives the same bits as the oracle."""
+    W, H, D, K = case
+    monkeypatch.setenv("STEREO_YPASS_V", "2")
+    L, R, _ = synth.scene(W, H, D, seed=12)
+    got = _run_gpu(L, R, D, k_scale=K)
+    monkeypatch.delenv("STEREO_YPASS_V")
+    ref = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "fixed", stages=("DL", "DR", "out"))
+    for s in ("DL", "DR"):
+        assert np.array_equal(got[s], ref[s])
+    assert np.array_equal(got["out"].view(np.uint32), ref["out"].view(np.uint32))
