@@ -281,15 +281,19 @@ def run_ours(args):
             dist.barrier()
 
     def run_frames(n, ns, c0=0):
-        """n frames as chunks of NB, chunk c on stream c % ns (the last chunk may be short)."""
-        c, done = c0, 0
-        while done < n:
-            k = c % ns
-            m = min(NB, n - done)
-            handles[k].compute_batch(Lc[c % nchunk][:m], Rc[c % nchunk][:m], out[k][:m], m,
-                                     stream=streams[k])
-            done += m
-            c += 1
+        """n frames over ns streams, as evenly as possible (so that the streams
+        finish together), each stream's share in chunks of NB frames (the last
+        chunk may be short); chunks issued round-robin over the streams."""
+        left = [n // ns + (1 if k < n % ns else 0) for k in range(ns)]
+        c = c0
+        while any(left):
+            for k in range(ns):
+                if left[k]:
+                    m = min(NB, left[k])
+                    handles[k].compute_batch(Lc[c % nchunk][:m], Rc[c % nchunk][:m], out[k][:m], m,
+                                             stream=streams[k])
+                    left[k] -= m
+                    c += 1
         return c
 
     def timed(nframes, ns, c0=0):

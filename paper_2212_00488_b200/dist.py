@@ -135,13 +135,13 @@ class BandRunner:
         return self.dist.batch_isend_irecv(ops) if ops else []
 
     def reduce_summaries(self):
-        """Element-wise MAX over the bands of the frame-wide row summaries."""
-        if self.P > 1:
-            if self.summ_dev is not self.summ:
-                self.summ.copy_(self.summ_dev)
-            self.dist.all_reduce(self.summ, op=self.dist.ReduceOp.MAX)
-            if self.summ_dev is not self.summ:
-                self.summ_dev.copy_(self.summ)
+        """Element-wise MAX over the bands of the frame-wide row summaries
+        (one NCCL all-reduce, stream-ordered: no host synchronisation)."""
+        if self.summ_dev is not self.summ:
+            self.summ.copy_(self.summ_dev)
+        self.dist.all_reduce(self.summ, op=self.dist.ReduceOp.MAX)
+        if self.summ_dev is not self.summ:
+            self.summ_dev.copy_(self.summ)
 
     # ---------------------------------------------------------------- compute
     def compute(self, slot, out_own, stream=None):

@@ -168,3 +168,44 @@ def test_stream_slices_partition():
     for n, P in ((256, 8), (10, 3), (7, 7)):
         got = sorted(i for r in range(P) for i in sdist.stream_slice(n, P, r))
         assert got == list(range(n))
+
+
+def _c4_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 11  # a short stream of the c4 kind (translating scene), split over the ranks
+        sl = sdist.stream_slice(n, world, rank)
+        mine = synth.stream(48, 32, 8, n, seed=4, idx=sl)
+        digests = [(i, int(np.asarray(L, np.int64).sum()), int(np.asarray(R, np.int64).sum()))
+                   for i, (L, R) in zip(sl, mine)]
+        parts = [None] * world
+        dist.all_gather_object(parts, digests)
+        if rank == 0:
+            full = synth.stream(48, 32, 8, n, seed=4)
+            ref = [(i, int(L.astype(np.int64).sum()), int(R.astype(np.int64).sum())) for i, (L, R) in enumerate(full)]
+            got = sorted(d for p in parts for d in p)
+            q.put(got == ref)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c4_stream_slices_render_the_whole_stream(world):
+    """Config c4: every rank renders only its dist.stream_slice of the frame
+    stream (synth.stream(idx=...)); together the ranks hold exactly the frames
+    of a whole-stream render, each once."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c4_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10)
