@@ -400,6 +400,7 @@ def run_ours(args):
                         f"these are {sha}")
                 prof = {}
         pipes = prof.get("pipes", {})
+        prof_nb = max(int(prof.get("frames_per_launch", 1)), 1)  # frames per launch of the capture
         aggregation = {}
         for k in ("xpass", "ypass"):
             us = stage_ms[k.upper()] / launches * 1e3
@@ -411,7 +412,7 @@ def run_ours(args):
             aggregation[k] = {"us_per_launch": us, "frames_per_launch": NB,
                               "algorithmic_bytes_per_launch": algb[k] * NB, "hbm_gbs": gbs,
                               "hbm_frac": gbs / peak, "ncu_dram_hbm_frac": ncu_frac,
-                              "ncu_pipes": pipes.get(k)}
+                              "ncu_frames_per_launch": prof_nb, "ncu_pipes": pipes.get(k)}
         step_ms = ms_max / args.steps
         line = {
             "metric": METRIC, "value": fps, "unit": "fps", "n_gpus": ws, "steps": args.steps,
@@ -430,7 +431,7 @@ def run_ours(args):
             "stage_us_per_frame": {k: v / max(nfr, 1) * 1e3 for k, v in stage_ms.items()},
             "roofline": {"kernel": dom.lower(), "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic * NB if traffic else None, "traffic_source": prov,
+                         "traffic": traffic * NB / prof_nb if traffic else None, "traffic_source": prov,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
                          "frames_per_launch": NB, "pipes": pipes.get(dom.lower())},
             "aggregation_kernels": aggregation,

@@ -7,7 +7,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr, units = rows[0], rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out = {"source": f"ncu --set full --clock-control none, report {os.path.basename(sys.argv[1])} ({sys.argv[2]})",
-       "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch (one frame per launch); writes still dirty in L2 at kernel end are not counted",
+       "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch; writes still dirty in L2 at kernel end are not counted",
+       "frames_per_launch": int(os.environ.get("QT_BATCH", "1")),
        "source_sha": bench._source_sha()}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
