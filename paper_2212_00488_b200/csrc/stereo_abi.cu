@@ -392,7 +392,6 @@ int create_impl(int W, int H, int D, const stereo_params* p, int nb, const BandG
   }
   build_tables(*p, g.f, h->qad_h, h->qmc_h);
   const size_t n = (size_t)g.Ws * g.Hs * nb;  // per-frame buffers x NB frames
-  const size_t N = (size_t)W * H * nb;
   const size_t vol = (size_t)((g.Ds + 1) / 2) * 2 * g.Hs * nb * g.Wp;  // disparity pairs (u32 x 2)
   Buffers& b = h->b;
   struct A { void** p; size_t bytes; } as[] = {
@@ -406,7 +405,6 @@ int create_impl(int W, int H, int D, const stereo_params* p, int nb, const BandG
       {(void**)&b.fill, n * 4}, {(void**)&b.qad, 256 * 4}, {(void**)&b.qmc, 7 * 4},
       {(void**)&b.qtab, (size_t)(256 + 64) * 32 * 4},
   };
-  (void)N;
   for (auto& a : as) {
     if ((rc = alloc(h, a.p, a.bytes))) { stereo_destroy(h); return rc; }
   }

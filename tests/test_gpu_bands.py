@@ -113,3 +113,32 @@ def test_c5_eight_bands_bit_exact():
     full = _full(L, R, 290)
     got, _ = _bands(L, R, 290, 8)
     assert np.array_equal(got.view(np.uint32), full.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_band_splits(seed):
+    """Random frames, parameters (delta, w_x, w_y, T, pool radius, census
+    pattern, fill mode) and band counts: the bands reassemble to the whole
+    frame bit for bit (the library's halo covers the cone; rule (d) from the
+    frame-wide summaries)."""
+    import oracle
+    rng = np.random.default_rng(500 + seed)
+    K = int(rng.choice([1, 2]))
+    W = int(rng.integers(8, 160))
+    H = int(rng.integers(12 * K, 140))
+    D = int(rng.integers(1, 40))
+    cand = [(dx, dy) for dx in range(-2, 3) for dy in range(-2, 3) if (dx, dy) != (0, 0)]
+    pat = [cand[i] for i in rng.choice(len(cand), 6, replace=False)]
+    kw = dict(k_scale=K, delta=int(rng.integers(1, 60)), w_x=int(rng.integers(0, 30)),
+              w_y=int(rng.integers(0, 40)), t_fill=int(rng.integers(0, 6)),
+              m_pool=int(rng.integers(0, 4)), census=pat, fill_mode=int(rng.integers(0, 4)))
+    if rng.random() < 0.5:
+        L, R, _ = synth.scene(W, H, max(D, 2), seed=seed)
+    else:
+        L, R = synth.random_pair(W, H, seed=seed, levels=int(rng.integers(2, 257)))
+    P = int(rng.integers(1, min(6, H // K) + 1))
+    full = _full(L, R, D, **kw)
+    ref = oracle.pipeline(L, R, D, oracle.params(**kw), "fixed", stages=("out",))["out"]
+    assert np.array_equal(full.view(np.uint32), ref.view(np.uint32))
+    got, _ = _bands(L, R, D, P, check_cone=False, **kw)
+    assert np.array_equal(got.view(np.uint32), full.view(np.uint32)), (W, H, D, P, kw)
