@@ -134,7 +134,8 @@ int stereo_create(int W, int H, int D, const stereo_params* p, stereo_t** out);
  * disparity in original-resolution pixels, range [0, K*(Ds-1)]; every pixel is
  * written, INVALID is never emitted.  L, R and disp_out stay owned by the
  * caller and must remain valid until the stream work completes.  A handle is
- * not re-entrant: use one handle per concurrently running stream. */
+ * not re-entrant: use one handle per concurrently running stream.
+ * STEREO_EINVAL for NULL pointers or a band handle (stereo_compute_band). */
 int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                    void* stream);
 
@@ -161,7 +162,9 @@ int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nf
  * (HOST f32 [H][W]), all enqueued on `stream`; returns without synchronising.
  * Host buffers should be page-locked (cudaHostAlloc / torch pin_memory) for
  * the copies to be asynchronous; the caller must synchronise the stream
- * before reading disp_out or reusing L/R. */
+ * before reading disp_out or reusing L/R.  The FIRST call on a handle
+ * allocates the device staging (6*W*H bytes, counted in device_bytes); later
+ * calls never allocate. */
 int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                         void* stream);
 
@@ -172,6 +175,7 @@ void stereo_destroy(stereo_t* h);
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* stereo_last_error(void);
 
+/* Derived sizes and resources of the handle (HOST struct). */
 int stereo_get_info(const stereo_t* h, stereo_info* info);
 
 /* Copy the handle's fixed-point tables to HOST arrays: qad[256] (indexed by
