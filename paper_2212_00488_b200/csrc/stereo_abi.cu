@@ -210,7 +210,11 @@ int enqueue_frames(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, 
   CU(launch_prep(g, h->plan, Ls, Rs, padded, b, nfr, s));
   mark(STEREO_STAGE_PREP);
   const Plan& p = h->plan;
-  if (p.l2_bands > 1 && !h->debug_ca) {
+  if (p.fused && !h->debug_ca) {
+    // NEXT-1 prototype: one kernel from the PREP outputs to D^L, D^R
+    CU(launch_fused(g, p, b, s));
+    mark(STEREO_STAGE_YPASS);
+  } else if (p.l2_bands > 1 && !h->debug_ca) {
     // L2 band staging (NEXT-1 prototype): x pass of band k's
     // rows (+ w_y rows ahead), then the y pass of band k's outputs, which
     // reads CA_x rows written moments before (L2 hits); rows no later band

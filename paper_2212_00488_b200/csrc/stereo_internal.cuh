@@ -88,6 +88,8 @@ struct Plan {
   int l2_bands = 0;  // > 1: C+CA_x / CA+WTA interleaved over this many row bands (NEXT-1 prototype)
   int l2_band_rows = 0;
   CUtensorMap tmL, tmR;  // 3-D u64 maps over the CA_x volumes {Wp, Hs, ceil(Ds/2)}
+  bool fused = false;   // NEXT-1 prototype: fused_kernel instead of the x and y passes
+  int fused_smem = 0;
   int post_smem = 0;
   int post_rows = 2;     // scaled rows per POST CTA
   int post_threads = 512;
@@ -114,6 +116,8 @@ cudaError_t launch_ypass_rows(const Geom& g, const Plan& p, Buffers& b, int y0, 
                               cudaStream_t s);
 cudaError_t launch_ypass(const Geom& g, const Plan& p, Buffers& b, bool store_ca, int nfr,
                          cudaStream_t s);
+// NEXT-1 prototype: cost + CA_x + CA + WTA in one kernel (CA_x stays on chip)
+cudaError_t launch_fused(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s);
 // band mode: out = the caller's band output (own original rows only)
 cudaError_t launch_post(const Geom& g, const Plan& p, Buffers& b, const uint8_t* Lorg,
                         float* out, int nfr, cudaStream_t s);

@@ -739,6 +739,201 @@ __global__ void __launch_bounds__(kYThreads, 2)
     if (r < nr && x < a.Ws) dmap[(size_t)(y0 + seg + 16 * r) * a.Ws + x] = (uint8_t)(__double2loint(best[r]) & 255);
 }
 
+// ============================================================================
+// FUSED (NEXT-1 prototype, STEREO_FUSED=1): cost + CA_x + CA + WTA in ONE
+// kernel, CA_x never leaves the SM.  The y stage is v1's (same tile, split
+// prefix, WTA); instead of a TMA load, the CTA computes its tile of CA_x
+// itself for each disparity pair: warp w takes tile rows w, w+8, ...; per row
+// the 64 cost columns [x0 - 24, x0 + 40) that the 16 output columns' x
+// windows can reach (w_x, w_x_r <= 24) -- Eqs. 3-5 from the PREP code words
+// and the bank-replicated fixed-point tables (BORDER outside the right /
+// left image, R12b) -- a warp-scan exclusive prefix into per-warp shared
+// scratch, then Eq. 7's window difference for the 16 columns (lanes 0-15:
+// d, lanes 16-31: d+1).  The right base evaluates its own costs
+// C^R(x', d) = C(x'+d, d) (Eq. 6): nothing is shared between the bases and
+// each output needs (16 + 48) / 16 x TB / B cost evaluations (vs 0.5 staged).
+// ============================================================================
+struct FArgs {
+  const uint32_t* xrow;  // [4][Hs][Wp]: code L, code R (census | I << 24)
+  const uint32_t* qtab;  // the replicated tables (40 KB)
+  uint32_t border;
+  int Wp;
+};
+constexpr int kFHalo = 24;  // max x arm of the fused prototype
+
+template <int SEG>
+__global__ void __launch_bounds__(kYThreads, 1)
+    fused_kernel(YArgs a, FArgs f) {
+  constexpr int TB = kYSegs * SEG;
+  extern __shared__ __align__(128) uint8_t ysm[];
+  uint32_t* sQAD = reinterpret_cast<uint32_t*>(ysm);          // [256][32]
+  uint32_t* sQMC = sQAD + 256 * 32;                           // [64][32]
+  uint32_t* tile = sQMC + 64 * 32;                            // [TB][16] x u64 (d, d+1)
+  uint2* Elo = reinterpret_cast<uint2*>(tile + 2 * TB * 16);   // [TB+1][16]
+  uint32_t* Ehi = reinterpret_cast<uint32_t*>(Elo + (TB + 1) * 16);
+  uint4* tot = reinterpret_cast<uint4*>(Ehi + (TB + 1) * 16); // [8][16]
+  uint32_t* scr = reinterpret_cast<uint32_t*>(tot + 8 * 16);  // [8 warps][2][65] row prefixes
+  uint64_t* bar = reinterpret_cast<uint64_t*>(scr + 8 * 2 * 72);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int col = tid & 15, seg = tid >> 4, upper = (tid >> 4) & 1;
+  const int base = blockIdx.z;
+  const uint32_t* armp = base ? a.arm1 : a.arm0;
+  uint8_t* dmap = base ? a.D1 : a.D0;
+  const int x0 = blockIdx.x * 16, x = x0 + col;
+  const int y0 = a.y_begin + blockIdx.y * a.B, yt0 = y0 - a.w_y;
+  const int Ds = a.Ds, Ws = a.Ws, Hs = a.Hs;
+  const size_t plane = (size_t)Hs * f.Wp;
+  const uint32_t* codeL = f.xrow;
+  const uint32_t* codeR = f.xrow + plane;
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    constexpr uint32_t kTabBytes = (256 + 64) * 32 * 4;
+    mbar_expect_tx(bar, kTabBytes);
+    bulk_g2s(sQAD, f.qtab, kTabBytes, bar);
+  }
+  __syncthreads();
+  if (tid < 16) {
+    Elo[tid] = make_uint2(0u, 0u);
+    Ehi[tid] = 0u;
+  }
+  const int nrow = min(a.B, a.y_end - y0);
+  const int nr = max(0, (nrow - seg + 15) >> 4);
+  const int nrw = max(nr, __shfl_xor_sync(kFull, nr, 16));
+  uint32_t oab[kYRPT];
+  double best[kYRPT];
+#pragma unroll
+  for (int r = 0; r < kYRPT; ++r) {
+    const int y = y0 + seg + 16 * r;
+    oab[r] = 0u;
+    best[r] = __hiloint2double(0x7ff00000, 0);
+    if (r < nr && x < Ws) {
+      const uint32_t arm = __ldg(armp + (size_t)y * Ws + x);
+      const int M = (arm >> 16) & 255u, N = arm >> 24;
+      oab[r] = (((uint32_t)(y - M - yt0) * 16u + col) * 8u) |
+               ((((uint32_t)(y + N + 1 - yt0) * 16u + col) * 8u) << 16);
+    }
+  }
+  mbar_wait(bar, 0u);
+  const char* qadb = reinterpret_cast<const char*>(sQAD + lane);
+  const char* qmcb = reinterpret_cast<const char*>(sQMC + lane);
+  const uint2* t01 = reinterpret_cast<const uint2*>(tile) + seg * SEG * 16 + col;
+  uint2* Ew = Elo + (seg * SEG + 1) * 16 + col;
+  uint32_t* Hw = Ehi + (seg * SEG + 1) * 16 + col;
+  uint32_t* sp = scr + w * 2 * 72;  // this warp's two prefix rows (d, d+1), 65 entries each
+  constexpr uint32_t kLoMask = (1u << kYSplit) - 1u;
+  const int cb = x0 - kFHalo;          // first cost column of the row window
+  const int c0 = cb + 2 * lane;        // this lane's two cost columns c0, c0 + 1
+
+#pragma unroll 1
+  for (int d = 0; d < Ds; d += 2) {
+    // ---- x stage: this pair's CA_x tile, rows yt0 .. yt0 + TB - 1
+    for (int r = w; r < TB; r += 8) {
+      const int yy = yt0 + r;
+      uint2* trow = reinterpret_cast<uint2*>(tile) + r * 16;
+      if (yy < 0 || yy >= Hs) {  // outside the image: zero rows (never inside a window)
+        if (lane < 16) trow[lane] = make_uint2(0u, 0u);
+        continue;
+      }
+      const uint32_t* cl = codeL + (size_t)yy * f.Wp;
+      const uint32_t* cr = codeR + (size_t)yy * f.Wp;
+      uint32_t cost[2][2];  // [column][disparity]
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = c0 + k;
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const int dd = d + n;
+          // left base: C(c, dd) = Q[L(c), R(c - dd)]; right base: C(c + dd, dd) = Q[L(c + dd), R(c)]
+          const int xl = base ? c + dd : c, xr = base ? c : c - dd;
+          const bool out = base ? (xl >= Ws) : (xr < 0);  // BORDER (R12b)
+          const uint32_t pl = __ldg(cl + clampi(xl, 0, Ws - 1));
+          const uint32_t pr = __ldg(cr + clampi(xr, 0, Ws - 1));
+          const uint32_t qa = *reinterpret_cast<const uint32_t*>(qadb + (__vabsdiffu4(pl, pr) >> 17));
+          const uint32_t qm = *reinterpret_cast<const uint32_t*>(qmcb + (((pl ^ pr) & 63u) << 7));
+          cost[k][n] = out ? f.border : qa + qm;
+        }
+      }
+      // exclusive prefix over the 64 columns (two per lane), both disparities
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const uint32_t loc = cost[0][n] + cost[1][n];
+        uint32_t inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const uint32_t ex = inc - loc;
+        sp[n * 72 + 2 * lane] = ex;
+        sp[n * 72 + 2 * lane + 1] = ex + cost[0][n];
+        if (lane == 31) sp[n * 72 + 64] = inc;
+      }
+      __syncwarp();
+      // Eq. 7: lanes 0-15 the window of column x0 + lane at d, lanes 16-31 at d + 1
+      {
+        const int j = lane & 15, n = lane >> 4, xx = x0 + j;
+        uint32_t v = 0u;
+        if (xx < Ws && d + n < Ds) {
+          const uint32_t arm = __ldg((base ? a.arm1 : a.arm0) + (size_t)yy * Ws + xx);
+          const int m = arm & 255u, nn = (arm >> 8) & 255u;
+          v = sp[n * 72 + j + kFHalo + nn + 1] - sp[n * 72 + j + kFHalo - m];
+        }
+        reinterpret_cast<uint32_t*>(trow + j)[n] = v;
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // (0) tile complete
+    // ---- y stage (v1): column prefix in split precision, then the WTA
+    uint32_t l0[SEG], l1[SEG], lh[SEG];
+    uint32_t a0 = 0, a1 = 0, ah = 0;
+#pragma unroll
+    for (int s = 0; s < SEG; ++s) {
+      const uint2 v = t01[s * 16];
+      a0 += v.x & kLoMask;
+      a1 += v.y & kLoMask;
+      ah += __byte_perm(v.x, 0u, 0x4443u) + __byte_perm(v.y, 0u, 0x4344u);
+      l0[s] = a0; l1[s] = a1; lh[s] = ah;
+    }
+    const uint32_t b0 = __shfl_sync(kFull, a0, col), b1 = __shfl_sync(kFull, a1, col),
+                   bh = __shfl_sync(kFull, ah, col);
+    if (upper) tot[w * 16 + col] = make_uint4(b0 + a0, b1 + a1, bh + ah, 0u);
+    __syncthreads();  // (1) tile consumed, warp totals visible
+    uint32_t o0 = upper ? b0 : 0u, o1 = upper ? b1 : 0u, oh = upper ? bh : 0u;
+#pragma unroll
+    for (int q = 0; q < kYThreads / 32 - 1; ++q) {
+      if (q < w) {
+        const uint4 t = tot[q * 16 + col];
+        o0 += t.x; o1 += t.y; oh += t.z;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < SEG; ++s) {
+      Ew[s * 16] = make_uint2(l0[s] + o0, l1[s] + o1);
+      Hw[s * 16] = lh[s] + oh;
+    }
+    __syncthreads();  // (2) column prefixes complete
+    const uint8_t* EloB = reinterpret_cast<const uint8_t*>(Elo);
+    const uint8_t* EhiB = reinterpret_cast<const uint8_t*>(Ehi);
+    if (d + 1 < Ds)
+      ypass_wta_n<true>(nrw, best, oab, EloB, EhiB, d, a.e52);
+    else
+      ypass_wta_n<false>(nrw, best, oab, EloB, EhiB, d, a.e52);
+    // (the next pair's E stores follow its barrier (0), which every warp
+    // reaches only after this WTA)
+  }
+#pragma unroll
+  for (int r = 0; r < kYRPT; ++r)
+    if (r < nr && x < Ws) dmap[(size_t)(y0 + seg + 16 * r) * Ws + x] = (uint8_t)(__double2loint(best[r]) & 255);
+}
+
+static int fused_smem_bytes(int SEG) {
+  const int TB = kYSegs * SEG;
+  return (256 + 64) * 32 * 4 + 2 * TB * 16 * 4 + (TB + 1) * 16 * 12 + 8 * 16 * 16 + 8 * 2 * 72 * 4 + 16;
+}
+
+
 // Wide-strip variant (v2): CTA = 32-column strip x B output rows, 16 warps,
 // warp w = tile row segment w (SEG rows) across all 32 columns.  Every warp
 // access of the prefix arrays then lies in ONE tile row (32 consecutive
@@ -889,6 +1084,23 @@ static int ypass2_smem_bytes(int SEG) {
     case 15: { constexpr int SS = 15; EXPR; } break;   \
     default: break;                                    \
   }
+
+cudaError_t launch_fused(const Geom& g, const Plan& p, Buffers& b, cudaStream_t s) {
+  YArgs a;
+  a.arm0 = b.armL; a.arm1 = b.armR;
+  a.D0 = b.DL; a.D1 = b.DR;
+  a.ca0 = a.ca1 = nullptr;
+  a.Ws = g.Ws; a.Hs = g.Hs; a.Ds = g.Ds; a.w_y = g.w_y; a.B = p.ypass_B;
+  a.y_begin = 0;
+  a.y_end = g.Hs;
+  a.e52 = kYExp52;
+  FArgs f{b.xrow, b.qtab, g.border, g.Wp};
+  dim3 grid((g.Ws + 15) / 16, (g.Hs + p.ypass_B - 1) / p.ypass_B, 2);
+  cudaError_t e = cudaErrorInvalidValue;
+  YPASS_DISPATCH(p.ypass_SEG, (fused_kernel<SS><<<grid, kYThreads, p.fused_smem, s>>>(a, f),
+                               e = cudaGetLastError()))
+  return e;
+}
 
 static int ypass_seg_for(int T, int ver) {
   const int need = (T + kYSegs - 1) / kYSegs;
@@ -1697,6 +1909,16 @@ cudaError_t plan_kernels(const Geom& g, Plan& p, Buffers& b, int device) {
     YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, false>, p.ypass_smem));
     if (e != cudaSuccess) return e;
     YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(ypass_kernel<SS, true>, p.ypass_smem));
+    if (e != cudaSuccess) return e;
+  }
+  // FUSED (NEXT-1 prototype): whole frames of a batch-capacity-1 handle whose x arms fit the
+  // 24-column halo; same tiles as the y pass
+  p.fused = !g.band && g.NB == 1 && g.w_x_max <= kFHalo && env_int("STEREO_FUSED", 0, 0, 1) == 1;
+  if (p.fused) {
+    p.fused_smem = fused_smem_bytes(p.ypass_SEG);
+    YPASS_DISPATCH(p.ypass_SEG, e = max_carveout(fused_kernel<SS>));
+    if (e != cudaSuccess) return e;
+    YPASS_DISPATCH(p.ypass_SEG, e = raise_smem(fused_kernel<SS>, p.fused_smem));
     if (e != cudaSuccess) return e;
   }
   // XPASS: one persistent CTA per SM, as many warps (<= 16) as shared memory allows

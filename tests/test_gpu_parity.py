@@ -642,3 +642,19 @@ def test_ypass_v2_wide_strips_bit_exact(case, monkeypatch):
     for s in ("DL", "DR"):
         assert np.array_equal(got[s], ref[s])
     assert np.array_equal(got["out"].view(np.uint32), ref["out"].view(np.uint32))
+
+
+@pytest.mark.parametrize("case", [(1436, 992, 145, 2, 0), (300, 200, 48, 1, 3), (131, 77, 33, 2, 5),
+                                  (64, 48, 16, 1, 7)])
+def test_fused_next1_bit_exact(case, monkeypatch):
+    """NEXT-1 prototype (STEREO_FUSED=1): cost + CA_x + CA + WTA in one
+    kernel, CA_x never written to global memory; every stage bit-exact."""
+    W, H, D, K, seed = case
+    monkeypatch.setenv("STEREO_FUSED", "1")
+    L, R, _ = synth.scene(W, H, D, seed=seed)
+    got = _run_gpu(L, R, D, k_scale=K)
+    monkeypatch.delenv("STEREO_FUSED")
+    ref = oracle.pipeline(L, R, D, oracle.params(k_scale=K), "fixed", stages=("DL", "DR", "out"))
+    for s in ("DL", "DR"):
+        assert np.array_equal(got[s], ref[s]), s
+    assert np.array_equal(got["out"].view(np.uint32), ref["out"].view(np.uint32))

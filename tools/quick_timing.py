@@ -31,6 +31,8 @@ vol = i.Ds * i.Hs * i.Ws * 4 * 2
 for k, v in t.items():
     us = v / nf * 1e3
     extra = ""
+    if us <= 0:
+        continue
     if k == "XPASS": extra = f"  write {vol/1e6:.0f} MB -> {vol/us/1e3:.0f} GB/s"
     if k == "YPASS": extra = f"  read {vol/1e6:.0f} MB -> {vol/us/1e3:.0f} GB/s"
     print(f"  {k:6s} {us:8.1f} us{extra}")
