@@ -160,6 +160,58 @@ def _cpu_baseline(budget_s=12.0):
             "gdisp_evals_per_s": fps * W * H * D / 1e9}
 
 
+def _oracle_timing_table():
+    """`--oracle-timing` (the CPU-baseline leg's full table, SURVEY §8(d) "oracle
+    timing beside it"): the oracle as it stands on the host cores -- c1, c2, c3
+    in fixed and double mode, all cores and one thread; c4 / c5 extrapolated
+    from c3 (labelled).  One JSON object (profiles/r02_oracle_timing.json)."""
+    import platform
+
+    import oracle
+    from paper_2212_00488_b200 import synth
+
+    def time_one(L, R, D_, K_, mode, nthreads, budget, max_runs):
+        p = oracle.params(k_scale=K_)
+        n, t0 = 0, time.perf_counter()
+        while True:
+            oracle.pipeline(L, R, D_, p, mode, nthreads=nthreads, stages=("out",))
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= budget or n >= max_runs:
+                return el / n
+
+    cpu = platform.processor()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    nc = _cores()
+    cfgs = {"c1": (64, 48, 16, 1, lambda: synth.shift_pair(64, 48, 5, seed=0)),
+            "c2": (450, 375, 64, 1, lambda: synth.scene(450, 375, 64, seed=1)[:2]),
+            "c3": (1436, 992, 145, 2, lambda: synth.scene(1436, 992, 145, seed=0)[:2])}
+    res = {"cpu": cpu, "cores": nc, "configs": {}}
+    for name, (W_, H_, D_, K_, gen) in cfgs.items():
+        L, R = gen()
+        row = {}
+        for mode in ("fixed", "double"):
+            for nt in (nc, 1):
+                if name == "c3" and nt == 1 and mode == "double":
+                    continue  # > a minute; the fixed one-thread figure stands for it
+                row[f"{mode}_threads{nt}_s_per_frame"] = time_one(
+                    L, R, D_, K_, mode, nt, budget=2.0 if nt == 1 else 6.0,
+                    max_runs=1 if (name == "c3" and nt == 1) else 20)
+        res["configs"][name] = row
+    c3 = res["configs"]["c3"]["fixed_threads%d_s_per_frame" % nc]
+    res["extrapolated"] = {"c4_256_frames_s": 256 * c3, "c5_one_frame_s": 8 * c3,
+                           "note": "c4 = 256 x c3; c5 = 8 x c3 (4x pixels, 2x disparities); "
+                                   "fixed mode, all cores; not measured"}
+    print(json.dumps(res, indent=1))
+    return 0
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -552,6 +604,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--oracle-timing", action="store_true",
+                    help="print the CPU oracle's timing table (c1-c3, both modes, all / one core) and exit")
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c3",
                     help="c3 (default, the driver's leg) and c1 / c2 / c4: frame batches; "
                          "c5: one high-res frame per step in row bands across the ranks")
@@ -573,6 +627,8 @@ def main():
     global W, H, D, K, WORKLOAD_NAME
     if args.workload in WORKLOADS:
         W, H, D, K, WORKLOAD_NAME = WORKLOADS[args.workload]
+    if args.oracle_timing:
+        return _oracle_timing_table()
     if args.impl == "reference":
         return run_reference(args)
     return run_c5_bands(args) if args.workload == "c5" else run_ours(args)
