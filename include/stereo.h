@@ -150,7 +150,8 @@ int stereo_compute(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_
 int stereo_create_batch(int W, int H, int D, const stereo_params* p, int max_frames,
                         stereo_t** out);
 
-/* `nframes` (>= 0) frames back to back; L, R: DEVICE u8 [nframes][H][W];
+/* `nframes` (>= 0; 0 is a no-op that accepts NULL buffers) frames back to
+ * back; L, R: DEVICE u8 [nframes][H][W];
  * disp_out: DEVICE f32 [nframes][H][W].  Processed in chunks of the handle's
  * max_frames, one launch sequence per chunk.  Same contract as
  * stereo_compute (enqueued on `stream`, no synchronisation, no allocation). */

@@ -549,8 +549,9 @@ int stereo_compute_rgb(stereo_t* h, const uint8_t* L_rgb, const uint8_t* R_rgb, 
 
 int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
                          float* disp_out, void* stream) {
-  if (!h || !L || !R || !disp_out || nframes < 0)
-    return fail(STEREO_EINVAL, "NULL handle/buffer or negative nframes");
+  if (!h || nframes < 0) return fail(STEREO_EINVAL, "NULL handle or negative nframes");
+  if (nframes == 0) return STEREO_OK;  // nothing to enqueue (buffers may be NULL)
+  if (!L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL buffer");
   if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
   DeviceGuard dg(h->device);
   const size_t in = (size_t)h->g.W * h->g.H;

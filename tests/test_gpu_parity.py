@@ -658,3 +658,22 @@ def test_fused_next1_bit_exact(case, monkeypatch):
     for s in ("DL", "DR"):
         assert np.array_equal(got[s], ref[s]), s
     assert np.array_equal(got["out"].view(np.uint32), ref["out"].view(np.uint32))
+
+
+def test_batch_handle_single_frame_calls():
+    """A handle of batch capacity 4 serves single frames too (stereo_compute,
+    stereo_compute_host use frame slot 0) and an empty batch is a no-op."""
+    W, H, D = 120, 90, 24
+    L, R, _ = synth.scene(W, H, D, seed=17)
+    ref = oracle.pipeline(L, R, D, oracle.params(), "fixed", stages=("out",))["out"]
+    st = abi.Stereo(W, H, D, max_frames=4)
+    out = torch.zeros((H, W), dtype=torch.float32, device=DEV)
+    st.compute(torch.from_numpy(L).to(DEV), torch.from_numpy(R).to(DEV), out)
+    oh = torch.zeros((H, W), dtype=torch.float32).pin_memory()
+    st.compute_host(torch.from_numpy(L).pin_memory(), torch.from_numpy(R).pin_memory(), oh)
+    e = torch.zeros((0, H, W), dtype=torch.uint8, device=DEV)
+    st.compute_batch(e, e, torch.zeros((0, H, W), dtype=torch.float32, device=DEV), 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(oh.numpy().view(np.uint32), ref.view(np.uint32))
+    st.close()
