@@ -209,3 +209,42 @@ def test_c4_stream_slices_render_the_whole_stream(world):
         p.join(timeout=300)
         assert p.exitcode == 0
     assert q.get(timeout=10)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_band_geometry_random_cases_with_oracle(seed):
+    """The library's band partition and halo (stereo_band_rows /
+    stereo_band_halo, host functions) on random shapes and parameters: the
+    oracle run on every band's sub-image reproduces the whole frame's own
+    rows bit for bit, once fill rule (d) is resolved from the frame-wide
+    summaries (what stereo_band_finish does)."""
+    rng = np.random.default_rng(900 + seed)
+    K = int(rng.choice([1, 2]))
+    W = int(rng.integers(6, 48))
+    H = int(rng.integers(8 * K, 90))
+    D = int(rng.integers(1, 12))
+    cand = [(dx, dy) for dx in range(-2, 3) for dy in range(-2, 3) if (dx, dy) != (0, 0)]
+    pat = [cand[i] for i in rng.choice(len(cand), 6, replace=False)]
+    ov = dict(k_scale=K, w_y=int(rng.integers(0, 12)), m_pool=int(rng.integers(0, 4)),
+              delta=int(rng.integers(1, 40)), w_x=int(rng.integers(0, 10)), census=pat)
+    L, R = synth.random_pair(W, H, seed=seed, levels=int(rng.integers(2, 257)))
+    P = int(rng.integers(1, min(5, H // K) + 1))
+    p = oracle.params(**ov)
+    full = oracle.pipeline(L, R, D, p, "fixed", stages=("median", "out"))
+    summ = _summaries(full["median"])
+    bands = sdist.band_layout(H, P, abi.default_params(**ov))
+    got = np.zeros_like(full["out"])
+    for b in bands:
+        Lb, Rb = L[b.sub_y0:b.sub_y0 + b.sub_rows], R[b.sub_y0:b.sub_y0 + b.sub_rows]
+        r = oracle.pipeline(Lb, Rb, D, p, "fixed", stages=("fill", "out"))
+        s0, ys0 = b.sub_y0 // K, b.y0 // K
+        ys1 = (b.y0 + b.rows) // K if b.y0 + b.rows < H else H // K
+        fill, out = r["fill"].copy(), r["out"]
+        hi = min(ys1 + (1 if K == 2 else 0), H // K)
+        patched = [y for y in range(ys0, hi) if summ[y, 0] < 0]
+        for y in patched:
+            fill[y - s0] = _rule_d_value(summ, y)
+        if patched:
+            out = fill if K == 1 else oracle.scale_up(fill, Lb, K, p.t_fill)
+        got[b.y0:b.y0 + b.rows] = out[b.top:b.top + b.rows]
+    assert np.array_equal(got.view(np.uint32), full["out"].view(np.uint32)), (W, H, D, P, ov)
