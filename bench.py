@@ -261,14 +261,18 @@ def run_reference(args):
     return 0
 
 
+KERNEL_SOURCES = ("stereo_kernels.cu", "stereo_xpass.cu", "stereo_internal.cuh", "stereo_common.cuh")
+
+
 def _source_sha():
-    """Digest of the kernel sources + build flags: ties an ncu capture to the
-    code being benched (profiles/ncu_traffic.json carries the one it saw)."""
+    """Digest of the kernel translation units + their headers + the build
+    flags (not the host-side ABI file): ties an ncu capture to the kernel code
+    being benched (profiles/ncu_traffic.json carries the one it saw)."""
     import hashlib
     h = hashlib.sha256()
     csrc = os.path.join(ROOT, "paper_2212_00488_b200", "csrc")
     for f in sorted(os.listdir(csrc)):
-        if f.endswith((".cu", ".cuh")):
+        if f in KERNEL_SOURCES:
             with open(os.path.join(csrc, f), "rb") as fh:
                 h.update(f.encode() + b"\0" + fh.read())
     import __graft_entry__ as ge

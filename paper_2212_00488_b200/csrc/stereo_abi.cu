@@ -192,7 +192,7 @@ int enqueue_frames(stereo_t* h, const uint8_t* L, const uint8_t* R, float* out, 
     cudaEventRecord(tf.ev[0], s);
   }
   auto mark = [&](int stage) {
-    if (!h->timing) return;
+    if (!h->timing || tf.n >= kMaxMarks) return;
     tf.stage[tf.n] = stage;
     tf.ev[tf.n + 1] = get_event(h);
     cudaEventRecord(tf.ev[tf.n + 1], s);
