@@ -2,19 +2,26 @@
 """Benchmark of the stereo hot path (BASELINE.json metric) — one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1|c2|c3|c4|c5] [--streams S] [--batch B]
+    python bench.py --oracle-timing
 
 A step is one pass of the whole hot path (SD -> census/arms -> C+CA_x ->
 CA+WTA -> CC+median -> fill -> SU) over one frame of BASELINE
 config c3 (1436x992, D=145, K=2 -> 718x496, D_s=73) on every GPU.  Inputs are
 synthetic Middlebury-shaped scenes (paper_2212_00488_b200.synth), a pool of 64
 distinct frames (182 MB > the 126 MB L2) resident in HBM before the timed
-region.  N > 1 (torchrun): every rank runs its own frames, no data-path
-collective (frames are independent: "scaling": "weak"); the time is the max
-over ranks of the CUDA-event time.
+region; the frames run as launch sequences of B frames (stereo_create_batch)
+on S streams, spread evenly so that the streams finish together (defaults per
+workload: the measured best, c3: 4 x 2).  N > 1 (torchrun): every rank runs
+its own frames (c4: its dist.stream_slice of a 256-frame stream), no
+data-path collective ("scaling": "weak"); the time is the max over ranks of
+the CUDA-event time.  --workload c5: one 2872x1984 frame per step in N row
+bands with the halo exchange of dist.BandRunner ("scaling": "strong").
 
 --impl reference times the CPU oracle (oracle/, fixed mode, all host cores) on
 the same config, each step a bounded sample (a band of rows of a c3 frame) so
-that the run stays within a few minutes.
+that the run stays within a few minutes; --oracle-timing prints the oracle's
+full timing table (c1-c3, both modes, all / one core).
 """
 from __future__ import annotations
 
