@@ -110,3 +110,41 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(abi, "_lib", None)
     with pytest.raises(abi.StereoLibraryError):
         abi.lib()
+
+
+def test_header_is_plain_c_and_host_calls_link(tmp_path):
+    """include/stereo.h compiles as C11 (no C++ constructs cross the boundary)
+    and a C program links against libstereo_b200.so and runs the host-only
+    calls (defaults, validation, the band partition and halo) without a GPU."""
+    src = tmp_path / "use.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "stereo.h"
+int main(void) {
+  stereo_params p;
+  stereo_default_params(&p);
+  if (p.abi_version != STEREO_ABI_VERSION || p.w_x != 21 || p.w_y != 31 || p.k_scale != 2) return 1;
+  int y0, rows, top, bot, total = 0;
+  for (int b = 0; b < 8; ++b) {
+    if (stereo_band_rows(992, &p, 8, b, &y0, &rows) != STEREO_OK) return 2;
+    if (y0 != total) return 3;
+    total += rows;
+    if (stereo_band_halo(992, &p, y0, rows, &top, &bot) != STEREO_OK) return 4;
+    if (y0 > 0 && top < 68) return 5;
+  }
+  if (total != 992) return 6;
+  stereo_t* h = 0;
+  p.lambda_ad = -1.0;  /* validation happens before any device call */
+  if (stereo_create(64, 48, 16, &p, &h) != STEREO_EINVAL || h) return 7;
+  printf("ok %s\n", stereo_last_error());
+  return 0;
+}
+''')
+    exe = tmp_path / "use"
+    libdir = os.path.dirname(abi.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        str(src), "-L", libdir, "-lstereo_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("ok lambda_ad"), (r.returncode, r.stdout, r.stderr)
