@@ -163,11 +163,20 @@ int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nf
  * (HOST f32 [H][W]), all enqueued on `stream`; returns without synchronising.
  * Host buffers should be page-locked (cudaHostAlloc / torch pin_memory) for
  * the copies to be asynchronous; the caller must synchronise the stream
- * before reading disp_out or reusing L/R.  The FIRST call on a handle
- * allocates the device staging (6*W*H bytes, counted in device_bytes); later
- * calls never allocate. */
+ * before reading disp_out or reusing L/R.  The FIRST host-buffer call on a
+ * handle allocates the device staging (6*W*H*max_frames bytes, counted in
+ * device_bytes); later calls never allocate. */
 int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                         void* stream);
+
+/* stereo_compute_host for `nframes` (>= 0; 0 is a no-op) frames back to
+ * back: HOST L, R u8 [nframes][H][W], HOST disp_out f32 [nframes][H][W]; per
+ * chunk of max_frames frames one copy in per image, one launch sequence, one
+ * copy out, all enqueued on `stream`; the first host-buffer call allocates
+ * the staging for max_frames frames (6*W*H*max_frames bytes).  Same rules as
+ * stereo_compute_host. */
+int stereo_compute_host_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
+                              float* disp_out, void* stream);
 
 /* Synchronise the device, then free every buffer and the handle.  NULL is a
  * no-op. */

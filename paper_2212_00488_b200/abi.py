@@ -42,6 +42,7 @@ EXPORTS = (
     "stereo_rgb_to_gray", "stereo_compute_rgb", "stereo_disparity_to_depth",
     "stereo_create_batch", "stereo_band_rows", "stereo_create_band", "stereo_band_halo",
     "stereo_compute_band", "stereo_band_summary", "stereo_band_finish",
+    "stereo_compute_host_batch",
 )
 
 
@@ -105,6 +106,7 @@ def lib():
             "stereo_compute": (i32, [vp, vp, vp, vp, vp]),
             "stereo_compute_batch": (i32, [vp, vp, vp, i32, vp, vp]),
             "stereo_compute_host": (i32, [vp, vp, vp, vp, vp]),
+            "stereo_compute_host_batch": (i32, [vp, vp, vp, i32, vp, vp]),
             "stereo_destroy": (None, [vp]),
             "stereo_last_error": (C.c_char_p, []),
             "stereo_get_info": (i32, [vp, C.POINTER(Info)]),
@@ -280,6 +282,15 @@ class Stereo:
         hw = (self.H, self.W)
         _check(lib().stereo_compute_host(self._h, _host(L, "L", "u8", hw), _host(R, "R", "u8", hw),
                                          _host(out, "out", "f32", hw), _stream_ptr(stream)))
+        return out
+
+    def compute_host_batch(self, L, R, out, nframes, stream=None):
+        """HOST u8 [n][H][W] x 2 -> HOST f32 [n][H][W]; per chunk of max_frames
+        frames one copy in, one launch sequence, one copy out."""
+        nhw = (nframes, self.H, self.W)
+        _check(lib().stereo_compute_host_batch(self._h, _host(L, "L", "u8", nhw), _host(R, "R", "u8", nhw),
+                                               nframes, _host(out, "out", "f32", nhw),
+                                               _stream_ptr(stream)))
         return out
 
     # ------------------------------------------------------------ debug / stages

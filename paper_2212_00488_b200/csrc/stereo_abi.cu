@@ -564,6 +564,24 @@ int stereo_compute_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nf
   return STEREO_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// device staging of the host-buffer calls: max_frames frames, allocated by
+// the first such call on the handle (never again)
+int host_staging(stereo_t* h) {
+  if (h->b.inL) return STEREO_OK;
+  const size_t in = (size_t)h->g.W * h->g.H * h->g.NB;
+  int rc;
+  if ((rc = alloc(h, (void**)&h->b.inL, in)) || (rc = alloc(h, (void**)&h->b.inR, in)) ||
+      (rc = alloc(h, (void**)&h->b.outF, in * 4)))
+    return rc;
+  return STEREO_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* disp_out,
                         void* stream) {
   if (!h || !L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL handle or buffer");
@@ -571,16 +589,35 @@ int stereo_compute_host(stereo_t* h, const uint8_t* L, const uint8_t* R, float* 
   DeviceGuard dg(h->device);
   const size_t in = (size_t)h->g.W * h->g.H;
   int rc;
-  if (!h->b.inL) {
-    if ((rc = alloc(h, (void**)&h->b.inL, in)) || (rc = alloc(h, (void**)&h->b.inR, in)) ||
-        (rc = alloc(h, (void**)&h->b.outF, in * 4)))
-      return rc;
-  }
+  if ((rc = host_staging(h))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   CU(cudaMemcpyAsync(h->b.inL, L, in, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->b.inR, R, in, cudaMemcpyHostToDevice, s));
   if ((rc = enqueue_frames(h, h->b.inL, h->b.inR, h->b.outF, 1, s))) return rc;
   CU(cudaMemcpyAsync(disp_out, h->b.outF, in * 4, cudaMemcpyDeviceToHost, s));
+  return STEREO_OK;
+}
+
+int stereo_compute_host_batch(stereo_t* h, const uint8_t* L, const uint8_t* R, int nframes,
+                              float* disp_out, void* stream) {
+  if (!h || nframes < 0) return fail(STEREO_EINVAL, "NULL handle or negative nframes");
+  if (nframes == 0) return STEREO_OK;
+  if (!L || !R || !disp_out) return fail(STEREO_EINVAL, "NULL buffer");
+  if (h->g.band) return fail(STEREO_EINVAL, "band handle: use stereo_compute_band");
+  DeviceGuard dg(h->device);
+  const size_t in = (size_t)h->g.W * h->g.H;
+  int rc;
+  if ((rc = host_staging(h))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  // per chunk of max_frames frames: one copy in per image, one launch
+  // sequence, one copy out (the staging is reused in stream order)
+  for (int i = 0; i < nframes; i += h->g.NB) {
+    const int nfr = std::min(h->g.NB, nframes - i);
+    CU(cudaMemcpyAsync(h->b.inL, L + i * in, nfr * in, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(h->b.inR, R + i * in, nfr * in, cudaMemcpyHostToDevice, s));
+    if ((rc = enqueue_frames(h, h->b.inL, h->b.inR, h->b.outF, nfr, s))) return rc;
+    CU(cudaMemcpyAsync(disp_out + i * in, h->b.outF, nfr * in * 4, cudaMemcpyDeviceToHost, s));
+  }
   return STEREO_OK;
 }
 

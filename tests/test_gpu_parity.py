@@ -677,3 +677,21 @@ def test_batch_handle_single_frame_calls():
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
     assert np.array_equal(oh.numpy().view(np.uint32), ref.view(np.uint32))
     st.close()
+
+
+@pytest.mark.parametrize("nb,n", [(1, 3), (3, 7), (4, 4)])
+def test_compute_host_batch_bit_exact(nb, n):
+    """stereo_compute_host_batch: pinned host frames in, host maps out, per
+    chunk of max_frames frames one copy in / launch sequence / copy out."""
+    W, H, D = 100, 70, 20
+    frames = [synth.scene(W, H, D, seed=60 + i)[:2] for i in range(n)]
+    st = abi.Stereo(W, H, D, max_frames=nb)
+    Lh = torch.from_numpy(np.stack([f[0] for f in frames])).pin_memory()
+    Rh = torch.from_numpy(np.stack([f[1] for f in frames])).pin_memory()
+    Oh = torch.zeros((n, H, W), dtype=torch.float32).pin_memory()
+    st.compute_host_batch(Lh, Rh, Oh, n)
+    torch.cuda.synchronize()
+    for k, (L, R) in enumerate(frames):
+        ref = oracle.pipeline(L, R, D, oracle.params(), "fixed", stages=("out",))["out"]
+        assert np.array_equal(Oh[k].numpy().view(np.uint32), ref.view(np.uint32)), k
+    st.close()
